@@ -1,0 +1,344 @@
+"""Pins for the float64 oracle (oracle/svoo.py) against things other than itself:
+the paper/SPEC worked examples (tests/golden), published test vectors, closed forms, library
+routines (scipy / torch SDPA / np.argsort) and brute force on tiny inputs.  CPU only."""
+import itertools
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import svoo
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+
+
+# ---------------------------------------------------------------- sampler (R4)
+def test_splitmix64_published_vector():
+    for case in GOLD["splitmix64"]:
+        s = case["seed"]
+        outs = []
+        for _ in range(len(case["out"])):
+            s, o = svoo.splitmix64_next(s)
+            outs.append(str(o))
+        assert outs == case["out"], case["cite"]
+
+
+@pytest.mark.parametrize("N,K", [(10, 10), (100, 1), (2048, 16), (5000, 1024)])
+def test_sample_distinct_sorted_in_range(N, K):
+    idx = svoo.sample_anchor_indices(N, K, seed=7, b=0, h=3, H=4, side=1)
+    assert idx.shape == (K,)
+    assert np.all(np.diff(idx) > 0)
+    assert idx[0] >= 0 and idx[-1] < N
+    if K == N:
+        assert np.array_equal(idx, np.arange(N))
+
+
+def test_sample_uniform_and_stream_separation():
+    N, K, T = 20, 5, 4000
+    cnt = np.zeros(N)
+    for s in range(T):
+        cnt[svoo.sample_anchor_indices(N, K, seed=s, b=0, h=0, H=1, side=0)] += 1
+    expected = T * K / N
+    chi2 = ((cnt - expected) ** 2 / expected).sum()
+    assert chi2 < 50, chi2          # 19 dof: p(chi2 > 50) ~ 1e-4
+    a = svoo.sample_anchor_indices(1000, 50, 1, 0, 0, 2, 0)
+    b = svoo.sample_anchor_indices(1000, 50, 1, 0, 0, 2, 1)
+    c = svoo.sample_anchor_indices(1000, 50, 1, 0, 1, 2, 0)
+    assert not np.array_equal(a, b) and not np.array_equal(a, c)
+
+
+# ---------------------------------------------------------------- numerics (golden)
+def test_softmax_golden():
+    for case in GOLD["softmax"]:
+        np.testing.assert_allclose(svoo.softmax_row(case["in"]), case["out"], rtol=0, atol=1e-15)
+
+
+def test_softmax_matches_scipy_and_shift_invariance():
+    from scipy.special import softmax
+    z = np.random.default_rng(0).normal(size=50) * 30
+    np.testing.assert_allclose(svoo.softmax_row(z), softmax(z), rtol=1e-13, atol=0)
+    np.testing.assert_allclose(svoo.softmax_row(z + 700), svoo.softmax_row(z), rtol=1e-12)
+
+
+def test_l2_normalize_golden():
+    for case in GOLD["l2_normalize"]:
+        np.testing.assert_allclose(svoo.l2_normalize_rows(case["in"]), case["out"], atol=1e-15)
+
+
+# ---------------------------------------------------------------- assignment (Alg. 1 Step A/B)
+def _explicit_distance_labels(X, Ca, Cs):
+    """Brute force: normalise with Python loops and compute ||a-b|| by explicit differences."""
+    def norm_rows(M):
+        out = []
+        for r in M:
+            n = math.sqrt(sum(float(v) * float(v) for v in r))
+            out.append([float(v) / n for v in r] if n > 0 else [float(v) for v in r])
+        return out
+    P = norm_rows([[sum(float(x[t]) * float(c[t]) for t in range(len(x))) for c in Ca] for x in X])
+    Pb = norm_rows([[sum(float(s[t]) * float(c[t]) for t in range(len(s))) for c in Ca] for s in Cs])
+    labels, dists = [], []
+    for p in P:
+        D = [math.sqrt(sum((p[t] - q[t]) ** 2 for t in range(len(p)))) for q in Pb]
+        best = min(range(len(D)), key=lambda j: (D[j], j))
+        labels.append(best)
+        dists.append(D)
+    return np.array(labels), np.array(dists)
+
+
+def test_assign_matches_explicit_differences():
+    rng = np.random.default_rng(1)
+    X, Ca, Cs = rng.normal(size=(40, 6)), rng.normal(size=(5, 6)), rng.normal(size=(7, 6))
+    r = svoo.assign_step(X, Ca, Cs)
+    lab, D = _explicit_distance_labels(X, Ca, Cs)
+    assert np.array_equal(r.labels, lab)
+    np.testing.assert_allclose(r.dist_best, D[np.arange(40), lab], atol=1e-12)
+
+
+def test_assign_identity_anchor_is_cosine_nearest_centroid():
+    """With C_anchor = I_d the step is the textbook cosine nearest-centroid rule (sklearn)."""
+    from sklearn.metrics.pairwise import cosine_similarity
+    rng = np.random.default_rng(2)
+    d = 16
+    X, Cs = rng.normal(size=(500, d)), rng.normal(size=(12, d))
+    r = svoo.assign_step(X, np.eye(d), Cs)
+    assert np.array_equal(r.labels, cosine_similarity(X, Cs).argmax(1))
+
+
+def test_assign_single_cluster_and_ties():
+    rng = np.random.default_rng(3)
+    X = rng.normal(size=(30, 4))
+    assert np.all(svoo.assign_step(X, rng.normal(size=(3, 4)), rng.normal(size=(1, 4))).labels == 0)
+    Cs = np.stack([np.ones(4), np.ones(4), -np.ones(4)])  # clusters 0 and 1 identical -> ties to 0
+    r = svoo.assign_step(X, np.eye(4), Cs)
+    assert not np.any(r.labels == 1)
+
+
+def test_reduced_form_agrees_with_literal():
+    """SURVEY §8c reduced form: argmin_j ||P^_i - Pbar^_j|| == argmax_j x_i . W_j,
+    W_j = Gamma c_j / ||Pbar_j||, Gamma = C_a^T C_a.  A different algebraic route (the one the
+    CUDA kernel uses), so a dropped normalisation or transposed operand in the oracle fails."""
+    rng = np.random.default_rng(4)
+    X, Ca, Cs = rng.normal(size=(3000, 32)), rng.normal(size=(20, 32)), rng.normal(size=(50, 32))
+    r = svoo.assign_step(X, Ca, Cs)
+    G = Ca.T @ Ca
+    W = (G @ Cs.T) / np.linalg.norm(Cs @ Ca.T, axis=1)[None, :]
+    red = (X @ W).argmax(1)
+    ok = r.gap > 1e-9
+    assert np.array_equal(r.labels[ok], red[ok])
+
+
+def test_planted_two_groups_bruteforce():
+    """n=8 keys in two well-separated groups, K=2: Step A recovers the planted partition, and
+    it is the best of all 2-partitions under the normalised-affinity scatter (brute force)."""
+    rng = np.random.default_rng(5)
+    d = 8
+    g0, g1 = rng.normal(size=d) * 3, rng.normal(size=d) * 3
+    truth = np.array([0, 0, 0, 0, 1, 1, 1, 1])
+    K = np.stack([(g0 if t == 0 else g1) + 0.05 * rng.normal(size=d) for t in truth])
+    Q = K + 0.05 * rng.normal(size=K.shape)
+    res = svoo.cocluster(Q, K, 2, 2, 3, init_q=np.array([0, 4]), init_k=np.array([1, 5]))
+    for lab in (res.Lk, res.Lq):
+        assert np.array_equal(lab, truth) or np.array_equal(lab, 1 - truth)
+    P = svoo.l2_normalize_rows(K @ res.Cq.T)
+
+    def scatter(lab):
+        s = 0.0
+        for c in (0, 1):
+            m = P[lab == c]
+            if len(m):
+                s += ((m - m.mean(0)) ** 2).sum()
+        return s
+    best = min((scatter(np.array(bits)), bits) for bits in itertools.product((0, 1), repeat=8)
+               if 0 < sum(bits) < 8)
+    assert np.array_equal(np.array(best[1]), truth) or np.array_equal(np.array(best[1]), 1 - truth)
+
+
+# ---------------------------------------------------------------- centroid update
+def test_update_is_member_mean_and_preserves_sum():
+    rng = np.random.default_rng(6)
+    X = rng.normal(size=(200, 5))
+    lab = rng.integers(0, 9, size=200)
+    lab[lab == 4] = 5                      # cluster 4 empty
+    prev = rng.normal(size=(9, 5))
+    C = svoo.update_centroids(X, lab, prev)
+    sizes = np.bincount(lab, minlength=9)
+    np.testing.assert_allclose((C * sizes[:, None]).sum(0), X.sum(0), atol=1e-11)
+    assert np.array_equal(C[4], prev[4])
+    for j in range(9):
+        if sizes[j]:
+            # the mean is the unique minimiser of sum ||x - c||^2: gradient zero
+            np.testing.assert_allclose((X[lab == j] - C[j]).sum(0), 0, atol=1e-11)
+
+
+# ---------------------------------------------------------------- permutation
+@pytest.mark.parametrize("K", [1, 7, 100])
+def test_counting_sort_matches_stable_argsort(K):
+    lab = np.random.default_rng(K).integers(0, K, size=5000)
+    lab[lab == (K // 2)] = 0 if K > 1 else lab[lab == 0]
+    perm, offs = svoo.counting_sort(lab, K)
+    assert np.array_equal(perm, np.argsort(lab, kind="stable"))
+    assert np.array_equal(offs, np.concatenate([[0], np.cumsum(np.bincount(lab, minlength=K))]))
+    assert np.array_equal(np.sort(perm), np.arange(len(lab)))
+
+
+# ---------------------------------------------------------------- selection
+def test_recall_count_golden():
+    for case in GOLD["recall_count"]:
+        assert svoo.recall_count(case["p"], case["tau"]) == case["count"], case["cite"]
+
+
+def test_recall_through_select_blocks():
+    """SPEC row [0.5,0.3,0.1,0.1] realised as softmax(Abar/sqrt(d)) with C_k = I."""
+    p = np.array([0.5, 0.3, 0.1, 0.1])
+    Cq = (2.0 * np.log(p))[None, :]       # d = 4 -> sqrt(d) = 2
+    r = svoo.select_blocks(Cq, np.eye(4), [5], [1, 1, 1, 1], 1.0, 0.8, 0.1, svoo.RULE_DENSITY)
+    assert r.c[0] == 2 and r.n_rec == 2
+
+
+def test_rho_rule_golden():
+    rules = {"as_written": svoo.RULE_AS_WRITTEN, "density": svoo.RULE_DENSITY}
+    for case in GOLD["rho_rule"]:
+        Kk = 10
+        n = svoo.rule_count(round(case["recall"] * Kk), case["budget"], case["theta"],
+                            rules[case["rule"]], Kk, Kk)
+        assert n == round(case["rho"] * Kk), case["cite"]
+
+
+def test_mask_golden():
+    for case in GOLD["mask"]:
+        row = np.array(case["row"])
+        k = len(row)
+        r = svoo.select_blocks(row[None, :], np.eye(k), [1], [1] * k, case["rho"], 0.95, 0.1,
+                               svoo.RULE_FIXED)
+        assert list(r.kept[0]) == case["kept"], case["cite"]
+
+
+def test_n_from_ratio_exact_decimals():
+    """R10: matches exact rational ceil(b*K) for every 3-decimal budget at K in {100, 500, 1024}."""
+    from fractions import Fraction
+    for Kk in (100, 500, 1024):
+        for m in range(1, 1001):
+            b = float(np.float32(m / 1000))
+            exact = math.ceil(Fraction(m, 1000) * Kk)
+            assert svoo.n_from_ratio(b, Kk) == min(max(exact, 1), Kk), (Kk, m)
+
+
+def test_masks_nested_and_full_budget():
+    rng = np.random.default_rng(8)
+    Cq, Ck = rng.normal(size=(6, 8)), rng.normal(size=(30, 8))
+    sk = np.ones(30, int)
+    sk[[3, 17]] = 0
+    prev = None
+    for b in (0.05, 0.2, 0.5, 0.9, 1.0):
+        r = svoo.select_blocks(Cq, Ck, np.ones(6), sk, b, 0.95, 0.1, svoo.RULE_FIXED)
+        assert not np.isin(r.kept, [3, 17]).any()
+        if prev is not None:
+            for a in range(6):
+                assert set(prev[a]) <= set(r.kept[a])
+        prev = r.kept
+    assert r.n_keep == 28
+
+
+# ---------------------------------------------------------------- attention
+def test_full_keep_equals_library_sdpa():
+    rng = np.random.default_rng(9)
+    for n in (8, 64, 256):
+        Q, K, V = rng.normal(size=(3, n, 16))
+        Lq = rng.integers(0, 3, n)
+        Lk = rng.integers(0, 4, n)
+        kept = np.tile(np.arange(4), (3, 1))
+        O = svoo.sparse_attention(Q, K, V, Lq, Lk, kept)
+        ref = torch.nn.functional.scaled_dot_product_attention(
+            torch.from_numpy(Q)[None], torch.from_numpy(K)[None], torch.from_numpy(V)[None])[0]
+        np.testing.assert_allclose(O, ref.numpy(), atol=1e-12)
+        np.testing.assert_allclose(svoo.dense_attention(Q, K, V), ref.numpy(), atol=1e-12)
+
+
+def test_singleton_blocks_pick_argmax_value():
+    """S:385 / S:422: singleton blocks -> Abar = Q K^T; keeping 1 block gives v[argmax_j q.k_j]."""
+    rng = np.random.default_rng(10)
+    n = 40
+    Q, K, V = rng.normal(size=(3, n, 8))
+    ones = np.ones(n, int)
+    r = svoo.select_blocks(Q, K, ones, ones, 1.0 / n, 0.95, 0.1, svoo.RULE_FIXED)
+    assert r.n_keep == 1
+    np.testing.assert_allclose(r.Abar, Q @ K.T, atol=1e-12)
+    O = svoo.sparse_attention(Q, K, V, np.arange(n), np.arange(n), r.kept)
+    np.testing.assert_allclose(O, V[(Q @ K.T).argmax(1)], atol=1e-12)
+
+
+def test_bruteforce_n8_masked_softmax():
+    rng = np.random.default_rng(11)
+    Q, K, V = rng.normal(size=(3, 8, 4))
+    Lq = np.array([0, 1, 0, 1, 1, 0, 0, 1])
+    Lk = np.array([0, 1, 2, 3, 0, 1, 2, 3])
+    kept = np.array([[0, 2], [1, 3]])
+    O = svoo.sparse_attention(Q, K, V, Lq, Lk, kept)
+    for i in range(8):
+        allowed = [j for j in range(8) if Lk[j] in kept[Lq[i]]]
+        w = [math.exp(sum(Q[i, t] * K[j, t] for t in range(4)) / 2.0) for j in allowed]
+        o = [sum(w[m] * V[allowed[m], t] for m in range(len(allowed))) / sum(w) for t in range(4)]
+        np.testing.assert_allclose(O[i], o, atol=1e-12)
+        assert np.all(O[i] >= V[allowed].min(0) - 1e-12) and np.all(O[i] <= V[allowed].max(0) + 1e-12)
+
+
+# ---------------------------------------------------------------- whole layer
+def _toy(seed=0, N_scale=1):
+    from synthetic import video_qkv
+    w = video_qkv(4, 8, 8 * N_scale, 1, 32, seed=seed)
+    f = lambda t: t[0, 0].double().numpy()
+    return f(w.q), f(w.k), f(w.v)
+
+
+def test_layer_full_budget_equals_dense():
+    Q, K, V = _toy()
+    r = svoo.coclust_sparse_attention_head(Q, K, V, 8, 12, 2, 3, 1.0, 0.95, 0.1, svoo.RULE_FIXED)
+    np.testing.assert_allclose(r.O, svoo.dense_attention(Q, K, V), atol=1e-12)
+
+
+def test_token_order_invariance():
+    Q, K, V = _toy(seed=1)
+    N = Q.shape[0]
+    pi = np.random.default_rng(12).permutation(N)      # new position p holds old token pi[p]
+    inv = np.argsort(pi)
+    iq = svoo.sample_anchor_indices(N, 8, 5, 0, 0, 1, 0)
+    ik = svoo.sample_anchor_indices(N, 12, 5, 0, 0, 1, 1)
+    a = svoo.cocluster(Q, K, 8, 12, 2, init_q=iq, init_k=ik)
+    b = svoo.cocluster(Q[pi], K[pi], 8, 12, 2, init_q=inv[iq], init_k=inv[ik])
+    assert np.array_equal(a.Lq[pi], b.Lq) and np.array_equal(a.Lk[pi], b.Lk)
+    np.testing.assert_allclose(a.Cq, b.Cq, atol=1e-12)
+    sa = svoo.select_blocks(a.Cq, a.Ck, np.bincount(a.Lq, minlength=8), np.bincount(a.Lk, minlength=12),
+                            0.3, 0.95, 0.1, svoo.RULE_DENSITY)
+    Oa = svoo.sparse_attention(Q, K, V, a.Lq, a.Lk, sa.kept)
+    Ob = svoo.sparse_attention(Q[pi], K[pi], V[pi], b.Lq, b.Lk, sa.kept)
+    np.testing.assert_allclose(Oa[pi], Ob, atol=1e-12)
+
+
+def test_assignment_halfstep_nonincreasing_and_optimal():
+    """With the centroids held fixed, each assignment is optimal (no token improves by switching),
+    hence the half-step objective cannot exceed that of the previous labels."""
+    Q, K, _ = _toy(seed=2)
+    res = svoo.cocluster(Q, K, 8, 12, 3, seed=1)
+    for t in res.trace:
+        X = K if t["side"] == "k" else Q
+        r = svoo.assign_step(X, t["C_anchor"], t["C_self"])
+        P = svoo.l2_normalize_rows(X @ t["C_anchor"].T)
+        Pb = svoo.l2_normalize_rows(t["C_self"] @ t["C_anchor"].T)
+        D = np.linalg.norm(P[:, None, :] - Pb[None, :, :], axis=2)
+        assert np.all(D[np.arange(len(X)), r.labels] <= D.min(1) + 1e-12)
+
+
+def test_toy_config_runs_fast():
+    import time
+    from synthetic import config_workload
+    w = config_workload("toy")
+    f = lambda t: t[0, 0].double().numpy()
+    t0 = time.time()
+    r = svoo.coclust_sparse_attention_head(f(w.q), f(w.k), f(w.v), 16, 16, 3, 0, 0.3, 0.95, 0.1,
+                                           svoo.RULE_DENSITY)
+    assert time.time() - t0 < 30
+    assert r.sel.n_keep >= 1 and r.O.shape == (2048, 64)
+    assert np.isfinite(r.O).all()
