@@ -1,0 +1,152 @@
+/*
+ * coclust.h — C ABI of libcoclust.so, the B200 (sm_100a) hot path of SVOO (arXiv 2603.18636):
+ * per-head online bidirectional co-clustering of queries and keys, cluster permutation,
+ * centroid-level block selection under a per-layer keep budget, and varlen block-sparse flash
+ * attention with the inverse permutation fused into its stores.
+ *
+ * Citations: "P:n" = /root/reference/PAPER.md line n (Alg. 1 = P:1203-1229, selection = P:1247-1257,
+ * kernels = P:1266); R1..R17 = the readings listed in DESIGN.md ("Readings of the paper").
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ * - Every pointer argument is a DEVICE pointer owned by the caller (the library never allocates,
+ *   frees or synchronises).  `stream` is a cudaStream_t passed as void*; every call only enqueues
+ *   work on it.  Calls are reentrant: no global mutable state.
+ * - Q, K, V, O are bf16 [B, H, N, d] given as (ptr, sb, sh, sn): element strides of the B, H and N
+ *   dimensions; the d dimension must be contiguous (stride 1).  Both [B,H,N,d] and [B,N,H,d]
+ *   buffers are expressible.  d must be 64 or 128.  ptr must be 16-byte aligned and sb, sh, sn
+ *   multiples of 8 elements (TMA).
+ * - "bh" below is b*H + h.  Labels are int32 in [0, k).  perm[bh][p] = the token at cluster-sorted
+ *   position p (stable: ascending token index inside a cluster); offs[bh][c]..offs[bh][c+1] are the
+ *   positions of cluster c (offs[bh][0] = 0, offs[bh][k] = N).
+ * - Centroids are fp32 [B, H, k, d] contiguous.
+ * - ws / ws_bytes: caller-owned scratch of at least cs_workspace_bytes(...) bytes, 256-byte
+ *   aligned.  Its contents are undefined between calls.
+ * - Errors: arguments are validated on the host BEFORE anything is enqueued; on error nothing is
+ *   launched and a cs_status != CS_OK is returned; cs_last_error() (thread-local) holds a message.
+ *   CS_ERR_CUDA reports a launch error; asynchronous device faults surface at the caller's next
+ *   synchronisation, as usual for CUDA.
+ * - Results are deterministic (no floating-point atomics) and independent of how many heads or
+ *   GPUs share a launch.
+ */
+#ifndef COCLUST_H
+#define COCLUST_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  CS_OK = 0,
+  CS_ERR_NULL = 1,        /* a required pointer is NULL                                       */
+  CS_ERR_SHAPE = 2,       /* B,H,N <= 0, d not in {64,128}, inconsistent strides               */
+  CS_ERR_ARG = 3,         /* k > N or k > 1024, iters < 1, tau not in (0,1], theta not in (0,1),
+                             scale <= 0, unknown rule                                           */
+  CS_ERR_ALIGN = 4,       /* pointer not 16-byte aligned or stride not a multiple of 8 elements */
+  CS_ERR_WORKSPACE = 5,   /* ws NULL or smaller than required                                  */
+  CS_ERR_UNSUPPORTED = 6, /* a size the kernels do not handle (e.g. N >= 2^24)                 */
+  CS_ERR_CUDA = 7         /* a CUDA launch / driver call failed                                */
+} cs_status;
+
+typedef struct { const void* ptr; int64_t sb, sh, sn; } cs_bf16_in;
+typedef struct { void* ptr; int64_t sb, sh, sn; } cs_bf16_out;
+
+/* The threshold-dependent rho rule, read per R8:
+ *   CS_RULE_DENSITY    budget[h] = d_hat (keep ratio):  n = min(n_rec, n_b) if 1-b > theta else max
+ *   CS_RULE_AS_WRITTEN budget[h] = s (sparsity, literal): n = min(n_rec, n_s) if s > theta else max
+ *   CS_RULE_FIXED      n = n_b (keep-ratio sweeps)
+ * with n_b = clamp(ceil(double(b)*k_k - 1e-3), 1, k_k) (R10), n_rec from Recall (R9), and the
+ * result clamped to [1, #nonempty key clusters].                                                 */
+typedef enum { CS_RULE_DENSITY = 0, CS_RULE_AS_WRITTEN = 1, CS_RULE_FIXED = 2 } cs_rule;
+
+/* Library version (major*10000 + minor*100 + patch). */
+int cs_version(void);
+/* Static text for a status code. */
+const char* cs_status_string(int status);
+/* Thread-local detail of the last error returned on this thread ("" if none). */
+const char* cs_last_error(void);
+
+/* Scratch bytes needed by any entry point below for these sizes (the maximum over entries). */
+size_t cs_workspace_bytes(int B, int H, int N, int d, int kq, int kk);
+
+/* ---------------------------------------------------------------------------------------------
+ * coclust_assign — Algorithm 1 for every (b,h), then the cluster permutation.
+ *   C_q^(0) = Q[Sample(N,kq)], C_k^(0) = K[Sample(N,kk)] (R4: Floyd sampling over splitmix64 with
+ *   stream seed seed ^ (((b*Ht+hg)*2+side) * 0x9E3779B97F4A7C15), side 0 = Q, 1 = K, where
+ *   hg = head_offset + h is the global head index and Ht = heads_total (0 -> H, head_offset must
+ *   then be 0) — so a head-sharded call reproduces the single-call streams bit for bit;
+ *   explicit index arrays init_q [B,H,kq] / init_k [B,H,kk] override the sampler when non-NULL);
+ *   iters times: Step A (keys; anchors C_q, self C_k) then Step B (queries; anchors the
+ *   new C_k, self the old C_q).  Assignment = argmin of the Euclidean distance
+ *   between L2-normalised affinity rows (R1-R3), evaluated in the exact reduced form
+ *   argmax_j x.W_j; ties -> lowest j.  Mean update in raw token space;
+ *   an empty cluster keeps its previous centroid (R5).
+ * Outputs: cq [B,H,kq,d], ck [B,H,kk,d] fp32 (post-update, R13); lq, lk int32 [B,H,N];
+ *   perm_q, perm_k int32 [B,H,N]; offs_q int32 [B,H,kq+1]; offs_k int32 [B,H,kk+1]. */
+cs_status coclust_assign(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in k, int kq, int kk,
+                         int iters, uint64_t seed, int head_offset, int heads_total,
+                         const int32_t* init_q, const int32_t* init_k,
+                         float* cq, float* ck, int32_t* lq, int32_t* lk, int32_t* perm_q,
+                         int32_t* offs_q, int32_t* perm_k, int32_t* offs_k, void* ws,
+                         size_t ws_bytes, void* stream);
+
+/* One assignment half-step of Alg. 1 with given centroids (parity helper):
+ * x [B,H,N,d] bf16; c_anchor [B,H,ka,d] fp32 (the other side's centroids); c_self [B,H,ks,d] fp32;
+ * labels out int32 [B,H,N].  ka, ks in [1,1024]. */
+cs_status coclust_assign_step(int B, int H, int N, int d, cs_bf16_in x, int ka,
+                              const float* c_anchor, int ks, const float* c_self,
+                              int32_t* labels, void* ws, size_t ws_bytes, void* stream);
+
+/* Centroid update "C <- Mean(X via L)": c_inout [B,H,k,d] fp32; rows of empty clusters
+ * are left unchanged (R5).  perm/offs as produced by coclust_permute.  If x_perm is non-NULL it
+ * also receives the cluster-sorted copy x_perm[bh][p][:] = x[b,h,perm[bh][p],:] (bf16,
+ * [B*H, N, d] contiguous). */
+cs_status coclust_update_centroids(int B, int H, int N, int d, cs_bf16_in x, int k,
+                                   const int32_t* perm, const int32_t* offs, float* c_inout,
+                                   void* x_perm, void* stream);
+
+/* Stable counting sort of labels [BH, N] into perm [BH, N] and offs [BH, k+1] (implied by the
+ * dynamic block-size kernels). */
+cs_status coclust_permute(int BH, int N, int k, const int32_t* labels, int32_t* perm,
+                          int32_t* offs, void* ws, size_t ws_bytes, void* stream);
+
+/* Top block-pair selection per (b,h):
+ *   Abar = C_q C_k^T in fp64 (columns of empty key clusters excluded, R9);
+ *   for each nonempty query block a: p = softmax(Abar_a / sqrt(d)) (R7),
+ *   c_a = min{m : sum of the m largest p >= tau - 1e-12} (R9, R9b), n_rec = ceil(sum c_a / Kq');
+ *   n from the rule (cs_rule, budget[h] float32, theta); kept[b][h][a][0..n) = the n key clusters
+ *   with largest raw Abar_a (ties -> lower index), ascending.  Entries past n are not written.
+ * budget [H] float32; tau in (0,1]; theta in (0,1).  n_keep out int32 [B,H]; kept out int32
+ * [B,H,kq,kk]. */
+cs_status block_select(int B, int H, int kq, int kk, int d, const float* cq, const float* ck,
+                       const int32_t* offs_q, const int32_t* offs_k, const float* budget,
+                       double tau, double theta, int rule, int32_t* n_keep, int32_t* kept,
+                       void* ws, size_t ws_bytes, void* stream);
+
+/* Block-sparse attention over the kept blocks:
+ *   for query i in cluster a: o_i = sum_{j: L_k(j) in kept[a]} softmax_j(q_i.k_j * scale) v_j,
+ * written in ORIGINAL token order (the inverse permutation is fused into the stores).  bf16 MMA,
+ * fp32 accumulation and softmax, bf16 P (R15).  scale > 0 (1/sqrt(d) for the paper). */
+cs_status block_sparse_attn(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in k, cs_bf16_in v,
+                            int kq, int kk, const int32_t* perm_q, const int32_t* offs_q,
+                            const int32_t* perm_k, const int32_t* offs_k, const int32_t* n_keep,
+                            const int32_t* kept, float scale, cs_bf16_out o, void* ws,
+                            size_t ws_bytes, void* stream);
+
+/* The whole layer: coclust_assign -> block_select -> block_sparse_attn, on device only (no host
+ * round trip; CUDA-graph capturable).  budget [H] is indexed by the local head h; head_offset /
+ * heads_total as in coclust_assign. */
+cs_status coclust_sparse_attention(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in k,
+                                   cs_bf16_in v, int kq, int kk, int iters, uint64_t seed,
+                                   int head_offset, int heads_total,
+                                   const float* budget, double tau, double theta, int rule,
+                                   float scale, cs_bf16_out o, void* ws, size_t ws_bytes,
+                                   void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* COCLUST_H */

@@ -1,0 +1,227 @@
+"""paper_2603_18636_b200 — B200 (sm_100a) hot path of SVOO (arXiv 2603.18636).
+
+Thin ctypes binding over libcoclust.so (include/coclust.h).  This module only marshals
+arguments: torch tensors provide device memory and the current CUDA stream; every step of the
+path runs in the library's CUDA kernels.  There is no CPU fallback: if the library or a CUDA
+device is missing, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+__all__ = [
+    "RULE_DENSITY", "RULE_AS_WRITTEN", "RULE_FIXED", "CoclustError", "lib", "workspace_bytes",
+    "Workspace", "coclust_assign", "coclust_assign_step", "coclust_update_centroids",
+    "coclust_permute", "block_select", "block_sparse_attn", "coclust_sparse_attention",
+]
+
+RULE_DENSITY, RULE_AS_WRITTEN, RULE_FIXED = 0, 1, 2
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libcoclust.so")
+
+
+class CoclustError(RuntimeError):
+    def __init__(self, status: int, name: str, msg: str):
+        super().__init__(f"{name}: {msg}")
+        self.status = status
+        self.name = name
+
+
+class _BF16In(ctypes.Structure):
+    _fields_ = [("ptr", ctypes.c_void_p), ("sb", ctypes.c_int64), ("sh", ctypes.c_int64),
+                ("sn", ctypes.c_int64)]
+
+
+class _BF16Out(ctypes.Structure):
+    _fields_ = [("ptr", ctypes.c_void_p), ("sb", ctypes.c_int64), ("sh", ctypes.c_int64),
+                ("sn", ctypes.c_int64)]
+
+
+_P = ctypes.c_void_p
+_I = ctypes.c_int
+_SIG = {
+    "cs_version": (_I, []),
+    "cs_status_string": (ctypes.c_char_p, [_I]),
+    "cs_last_error": (ctypes.c_char_p, []),
+    "cs_workspace_bytes": (ctypes.c_size_t, [_I, _I, _I, _I, _I, _I]),
+    "coclust_assign": (_I, [_I, _I, _I, _I, _BF16In, _BF16In, _I, _I, _I, ctypes.c_uint64, _I, _I, _P, _P,
+                            _P, _P, _P, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P]),
+    "coclust_assign_step": (_I, [_I, _I, _I, _I, _BF16In, _I, _P, _I, _P, _P, _P, ctypes.c_size_t, _P]),
+    "coclust_update_centroids": (_I, [_I, _I, _I, _I, _BF16In, _I, _P, _P, _P, _P, _P]),
+    "coclust_permute": (_I, [_I, _I, _I, _P, _P, _P, _P, ctypes.c_size_t, _P]),
+    "block_select": (_I, [_I, _I, _I, _I, _I, _P, _P, _P, _P, _P, ctypes.c_double, ctypes.c_double,
+                          _I, _P, _P, _P, ctypes.c_size_t, _P]),
+    "block_sparse_attn": (_I, [_I, _I, _I, _I, _BF16In, _BF16In, _BF16In, _I, _I, _P, _P, _P, _P, _P,
+                               _P, ctypes.c_float, _BF16Out, _P, ctypes.c_size_t, _P]),
+    "coclust_sparse_attention": (_I, [_I, _I, _I, _I, _BF16In, _BF16In, _BF16In, _I, _I, _I,
+                                      ctypes.c_uint64, _I, _I, _P, ctypes.c_double, ctypes.c_double, _I,
+                                      ctypes.c_float, _BF16Out, _P, ctypes.c_size_t, _P]),
+}
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libcoclust.so (raises if it was not built: `python -m paper_2603_18636_b200.build`)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built; run `python -m paper_2603_18636_b200.build`")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in _SIG.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(status: int):
+    if status != 0:
+        L = lib()
+        raise CoclustError(status, L.cs_status_string(status).decode(), L.cs_last_error().decode())
+
+
+def _stream(t: torch.Tensor) -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream(t.device).cuda_stream)
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _bf16(t: torch.Tensor, out: bool = False):
+    if t.dtype != torch.bfloat16 or t.dim() != 4 or t.stride(3) != 1:
+        raise ValueError("expected a bf16 [B, H, N, d] tensor with contiguous d")
+    cls = _BF16Out if out else _BF16In
+    return cls(t.data_ptr(), t.stride(0), t.stride(1), t.stride(2))
+
+
+def _cuda(t: torch.Tensor, name: str):
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (no CPU fallback)")
+
+
+def workspace_bytes(B, H, N, d, kq, kk) -> int:
+    return int(lib().cs_workspace_bytes(B, H, N, d, kq, kk))
+
+
+class Workspace:
+    """Grow-only device scratch buffer (caller-owned memory for the C ABI)."""
+
+    def __init__(self):
+        self.buf = None
+
+    def get(self, nbytes: int, device) -> torch.Tensor:
+        if self.buf is None or self.buf.numel() < nbytes or self.buf.device != torch.device(device):
+            self.buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+        return self.buf
+
+
+_default_ws = Workspace()
+
+
+def _ws(ws, nbytes, device):
+    w = (ws or _default_ws).get(nbytes, device)
+    return ctypes.c_void_p(w.data_ptr()), ctypes.c_size_t(w.numel())
+
+
+def coclust_assign(q, k, kq, kk, iters, seed=0, init_q=None, init_k=None, ws=None,
+                   head_offset=0, heads_total=0):
+    """Algorithm 1 for every (b,h) + final permutation.  Returns a dict of device tensors."""
+    _cuda(q, "q")
+    B, H, N, d = q.shape
+    dev = q.device
+    i32 = dict(dtype=torch.int32, device=dev)
+    r = dict(cq=torch.empty(B, H, kq, d, dtype=torch.float32, device=dev),
+             ck=torch.empty(B, H, kk, d, dtype=torch.float32, device=dev),
+             lq=torch.empty(B, H, N, **i32), lk=torch.empty(B, H, N, **i32),
+             perm_q=torch.empty(B, H, N, **i32), offs_q=torch.empty(B, H, kq + 1, **i32),
+             perm_k=torch.empty(B, H, N, **i32), offs_k=torch.empty(B, H, kk + 1, **i32))
+    w, wn = _ws(ws, workspace_bytes(B, H, N, d, kq, kk), dev)
+    _check(lib().coclust_assign(B, H, N, d, _bf16(q), _bf16(k), kq, kk, iters, seed, head_offset,
+                                heads_total, _ptr(init_q),
+                                _ptr(init_k), _ptr(r["cq"]), _ptr(r["ck"]), _ptr(r["lq"]),
+                                _ptr(r["lk"]), _ptr(r["perm_q"]), _ptr(r["offs_q"]),
+                                _ptr(r["perm_k"]), _ptr(r["offs_k"]), w, wn, _stream(q)))
+    return r
+
+
+def coclust_assign_step(x, c_anchor, c_self, ws=None, labels=None):
+    """One Alg. 1 assignment half-step: labels [B,H,N] int32."""
+    _cuda(x, "x")
+    B, H, N, d = x.shape
+    ka, ks = c_anchor.shape[2], c_self.shape[2]
+    labels = torch.empty(B, H, N, dtype=torch.int32, device=x.device) if labels is None else labels
+    w, wn = _ws(ws, workspace_bytes(B, H, N, d, ka, ks), x.device)
+    _check(lib().coclust_assign_step(B, H, N, d, _bf16(x), ka, _ptr(c_anchor.contiguous()), ks,
+                                     _ptr(c_self.contiguous()), _ptr(labels), w, wn, _stream(x)))
+    return labels
+
+
+def coclust_update_centroids(x, perm, offs, c_inout, x_perm=None):
+    _cuda(x, "x")
+    B, H, N, d = x.shape
+    k = c_inout.shape[2]
+    _check(lib().coclust_update_centroids(B, H, N, d, _bf16(x), k, _ptr(perm), _ptr(offs),
+                                          _ptr(c_inout), _ptr(x_perm), _stream(x)))
+    return c_inout
+
+
+def coclust_permute(labels, k, ws=None):
+    """labels [..., N] int32 -> (perm [..., N], offs [..., k+1])."""
+    _cuda(labels, "labels")
+    N = labels.shape[-1]
+    BH = labels.numel() // N
+    perm = torch.empty_like(labels)
+    offs = torch.empty(*labels.shape[:-1], k + 1, dtype=torch.int32, device=labels.device)
+    w, wn = _ws(ws, BH * ((N + 1023) // 1024) * k * 4 + 4096, labels.device)
+    _check(lib().coclust_permute(BH, N, k, _ptr(labels), _ptr(perm), _ptr(offs), w, wn,
+                                 _stream(labels)))
+    return perm, offs
+
+
+def block_select(cq, ck, offs_q, offs_k, budget, tau=0.95, theta=0.1, rule=RULE_DENSITY, ws=None):
+    """-> (n_keep [B,H] int32, kept [B,H,kq,kk] int32; first n_keep entries per row valid)."""
+    _cuda(cq, "cq")
+    B, H, kq, d = cq.shape
+    kk = ck.shape[2]
+    n_keep = torch.empty(B, H, dtype=torch.int32, device=cq.device)
+    kept = torch.full((B, H, kq, kk), -1, dtype=torch.int32, device=cq.device)
+    w, wn = _ws(ws, B * H * kq * (kk + 1) * 4 + 4096, cq.device)
+    _check(lib().block_select(B, H, kq, kk, d, _ptr(cq.contiguous()), _ptr(ck.contiguous()),
+                              _ptr(offs_q), _ptr(offs_k), _ptr(budget), float(tau), float(theta),
+                              int(rule), _ptr(n_keep), _ptr(kept), w, wn, _stream(cq)))
+    return n_keep, kept
+
+
+def block_sparse_attn(q, k, v, perm_q, offs_q, perm_k, offs_k, n_keep, kept, scale=None,
+                      out=None, ws=None):
+    _cuda(q, "q")
+    B, H, N, d = q.shape
+    kq, kk = offs_q.shape[-1] - 1, offs_k.shape[-1] - 1
+    scale = d ** -0.5 if scale is None else scale
+    out = torch.empty(B, H, N, d, dtype=torch.bfloat16, device=q.device) if out is None else out
+    w, wn = _ws(ws, workspace_bytes(B, H, N, d, kq, kk), q.device)
+    _check(lib().block_sparse_attn(B, H, N, d, _bf16(q), _bf16(k), _bf16(v), kq, kk, _ptr(perm_q),
+                                   _ptr(offs_q), _ptr(perm_k), _ptr(offs_k), _ptr(n_keep),
+                                   _ptr(kept), float(scale), _bf16(out, True), w, wn, _stream(q)))
+    return out
+
+
+def coclust_sparse_attention(q, k, v, kq, kk, iters, budget, *, seed=0, tau=0.95, theta=0.1,
+                             rule=RULE_DENSITY, scale=None, out=None, ws=None, head_offset=0,
+                             heads_total=0):
+    """The whole SVOO attention layer (north_star stages 1-5) on device."""
+    _cuda(q, "q")
+    B, H, N, d = q.shape
+    scale = d ** -0.5 if scale is None else scale
+    out = torch.empty(B, H, N, d, dtype=torch.bfloat16, device=q.device) if out is None else out
+    w, wn = _ws(ws, workspace_bytes(B, H, N, d, kq, kk), q.device)
+    _check(lib().coclust_sparse_attention(B, H, N, d, _bf16(q), _bf16(k), _bf16(v), kq, kk, iters,
+                                          seed, head_offset, heads_total, _ptr(budget), float(tau), float(theta), int(rule),
+                                          float(scale), _bf16(out, True), w, wn, _stream(q)))
+    return out

@@ -1,0 +1,459 @@
+// api.cu — the C ABI of libcoclust.so (include/coclust.h): host-side validation, workspace
+// carving, TMA descriptor encoding and the launch sequences.  No entry point allocates, frees or
+// synchronises; every launch goes to the caller's stream.
+#include <cuda.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+
+#include "../../include/coclust.h"
+#include "kernels.cuh"
+
+using namespace cs;
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+cs_status fail(cs_status s, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return s;
+}
+cs_status cuda_fail(cudaError_t e, const char* where) {
+  return fail(CS_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+#define CS_CUDA(call, where)                          \
+  do {                                                \
+    cudaError_t _e = (call);                          \
+    if (_e != cudaSuccess) return cuda_fail(_e, where); \
+  } while (0)
+#define CS_CHECK(expr)             \
+  do {                             \
+    cs_status _s = (expr);         \
+    if (_s != CS_OK) return _s;    \
+  } while (0)
+
+// ---------------------------------------------------------------- workspace carving
+struct Carve {
+  uint8_t* base;  // nullptr -> sizing pass
+  size_t off = 0;
+  explicit Carve(void* b) : base(static_cast<uint8_t*>(b)) {}
+  template <typename T>
+  T* take(size_t count) {
+    off = (off + 255) & ~size_t(255);
+    T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off += count * sizeof(T);
+    return p;
+  }
+};
+
+int round_up(int x, int m) { return (x + m - 1) / m * m; }
+int chunk_n(int ks) { return ks <= 256 ? round_up(ks, 16) : 256; }
+int pad_k(int ks) {
+  const int n = chunk_n(ks);
+  return (ks + n - 1) / n * n;
+}
+
+struct AssignScratch {
+  double* gamma;
+  __nv_bfloat16* wsplit;
+  int32_t* hist;
+};
+AssignScratch carve_assign(Carve& c, int BH, int N, int d, int kq, int kk) {
+  AssignScratch s;
+  const int kmax = std::max(kq, kk);
+  s.gamma = c.take<double>((size_t)BH * d * d);
+  s.wsplit = c.take<__nv_bfloat16>((size_t)BH * std::max(pad_k(kq), pad_k(kk)) * 2 * d);
+  s.hist = c.take<int32_t>((size_t)BH * ((N + kSortTile - 1) / kSortTile) * kmax);
+  return s;
+}
+struct SelectScratch {
+  int32_t* order;
+  int32_t* cnt;
+};
+SelectScratch carve_select(Carve& c, int BH, int kq, int kk) {
+  SelectScratch s;
+  s.order = c.take<int32_t>((size_t)BH * kq * kk);
+  s.cnt = c.take<int32_t>((size_t)BH * kq);
+  return s;
+}
+struct AttnScratch {
+  __nv_bfloat16 *qp, *kp, *vp;
+  int32_t* item_start;
+};
+AttnScratch carve_attn(Carve& c, int BH, int N, int d, int kq) {
+  AttnScratch s;
+  s.qp = c.take<__nv_bfloat16>((size_t)BH * N * d);
+  s.kp = c.take<__nv_bfloat16>((size_t)BH * N * d);
+  s.vp = c.take<__nv_bfloat16>((size_t)BH * N * d);
+  s.item_start = c.take<int32_t>((size_t)BH * (kq + 1));
+  return s;
+}
+struct LayerState {
+  float *cq, *ck;
+  int32_t *lq, *lk, *perm_q, *perm_k, *offs_q, *offs_k, *n_keep, *kept;
+};
+LayerState carve_state(Carve& c, int BH, int N, int d, int kq, int kk) {
+  LayerState s;
+  s.cq = c.take<float>((size_t)BH * kq * d);
+  s.ck = c.take<float>((size_t)BH * kk * d);
+  s.lq = c.take<int32_t>((size_t)BH * N);
+  s.lk = c.take<int32_t>((size_t)BH * N);
+  s.perm_q = c.take<int32_t>((size_t)BH * N);
+  s.perm_k = c.take<int32_t>((size_t)BH * N);
+  s.offs_q = c.take<int32_t>((size_t)BH * (kq + 1));
+  s.offs_k = c.take<int32_t>((size_t)BH * (kk + 1));
+  s.n_keep = c.take<int32_t>((size_t)BH);
+  s.kept = c.take<int32_t>((size_t)BH * kq * kk);
+  return s;
+}
+
+size_t need_assign(int BH, int N, int d, int kq, int kk) {
+  Carve c(nullptr);
+  carve_assign(c, BH, N, d, kq, kk);
+  return c.off + 256;
+}
+size_t need_select(int BH, int kq, int kk) {
+  Carve c(nullptr);
+  carve_select(c, BH, kq, kk);
+  return c.off + 256;
+}
+size_t need_attn(int BH, int N, int d, int kq) {
+  Carve c(nullptr);
+  carve_attn(c, BH, N, d, kq);
+  return c.off + 256;
+}
+size_t need_layer(int BH, int N, int d, int kq, int kk) {
+  Carve c(nullptr);
+  carve_state(c, BH, N, d, kq, kk);
+  carve_attn(c, BH, N, d, kq);
+  carve_assign(c, BH, N, d, kq, kk);
+  carve_select(c, BH, kq, kk);
+  return c.off + 256;
+}
+
+// ---------------------------------------------------------------- validation
+cs_status check_dims(int B, int H, int N, int d) {
+  if (B <= 0 || H <= 0 || N <= 0) return fail(CS_ERR_SHAPE, "B, H, N must be positive (got %d, %d, %d)", B, H, N);
+  if (d != 64 && d != 128) return fail(CS_ERR_SHAPE, "d must be 64 or 128 (got %d)", d);
+  if (N >= (1 << 24)) return fail(CS_ERR_UNSUPPORTED, "N must be < 2^24 (got %d)", N);
+  if ((long long)B * H * N >= (1LL << 31)) return fail(CS_ERR_UNSUPPORTED, "B*H*N must be < 2^31");
+  return CS_OK;
+}
+cs_status check_k(int k, int N, const char* name) {
+  if (k < 1 || k > N || k > kMaxClusters)
+    return fail(CS_ERR_ARG, "%s must be in [1, min(N, %d)] (got %d, N=%d)", name, kMaxClusters, k, N);
+  return CS_OK;
+}
+cs_status check_bf16(const void* ptr, int64_t sb, int64_t sh, int64_t sn, const char* name) {
+  if (!ptr) return fail(CS_ERR_NULL, "%s.ptr is NULL", name);
+  if (reinterpret_cast<uintptr_t>(ptr) % 16) return fail(CS_ERR_ALIGN, "%s.ptr not 16-byte aligned", name);
+  if (sb < 0 || sh < 0 || sn < 0) return fail(CS_ERR_SHAPE, "%s strides must be non-negative", name);
+  if (sb % 8 || sh % 8 || sn % 8)
+    return fail(CS_ERR_ALIGN, "%s strides must be multiples of 8 elements (got %lld, %lld, %lld)", name,
+                (long long)sb, (long long)sh, (long long)sn);
+  return CS_OK;
+}
+cs_status check_ws(void* ws, size_t have, size_t need) {
+  if (!ws) return fail(CS_ERR_WORKSPACE, "workspace is NULL (need %zu bytes)", need);
+  if (have < need) return fail(CS_ERR_WORKSPACE, "workspace too small: %zu < %zu bytes", have, need);
+  return CS_OK;
+}
+#define NEED(p, name) \
+  if (!(p)) return fail(CS_ERR_NULL, "%s is NULL", name)
+
+XView view(cs_bf16_in t, int H) { return XView{static_cast<const __nv_bfloat16*>(t.ptr), t.sb, t.sh, t.sn, H}; }
+
+// ---------------------------------------------------------------- TMA descriptors
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                                  CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                  CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+// 2D bf16 map over a row-major [rows, cols] matrix, box {64, box_rows}, SWIZZLE_128B.
+cs_status make_map_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return fail(CS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (no CUDA driver?)");
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(CS_ERR_CUDA, "cuTensorMapEncodeTiled (2D) failed: %d", (int)r);
+  return CS_OK;
+}
+// 4D bf16 map over a strided [B, H, N, d] tensor, box {64, 128, 1, 1}, SWIZZLE_128B.
+cs_status make_map_x(CUtensorMap* m, cs_bf16_in x, int B, int H, int N, int d) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return fail(CS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (no CUDA driver?)");
+  cuuint64_t dims[4] = {(cuuint64_t)d, (cuuint64_t)N, (cuuint64_t)H, (cuuint64_t)B};
+  cuuint64_t strides[3] = {(cuuint64_t)x.sn * 2, (cuuint64_t)std::max<int64_t>(x.sh, 8) * 2,
+                           (cuuint64_t)std::max<int64_t>(x.sb, 8) * 2};
+  cuuint32_t box[4] = {64, 128, 1, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x.ptr), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(CS_ERR_CUDA, "cuTensorMapEncodeTiled (4D) failed: %d", (int)r);
+  return CS_OK;
+}
+
+// ---------------------------------------------------------------- launch sequences
+cs_status run_assign_step(int B, int H, int N, int d, cs_bf16_in x, int ka, const float* ca, int ks,
+                          const float* cself, int32_t* labels, const AssignScratch& sc, cudaStream_t st) {
+  const int BH = B * H;
+  const int nch = chunk_n(ks), ks_pad = pad_k(ks);
+  CS_CUDA(launch_anchor_prep(ca, ka, cself, ks, ks_pad, BH, d, sc.gamma, sc.wsplit, st), "anchor_prep");
+  CUtensorMap tx, tw;
+  CS_CHECK(make_map_x(&tx, x, B, H, N, d));
+  CS_CHECK(make_map_2d(&tw, sc.wsplit, (uint64_t)BH * ks_pad, 2 * d, nch));
+  CS_CUDA(launch_assign_gemm(&tx, &tw, B, H, N, d, ks, nch, ks_pad, labels, st), "assign_gemm");
+  return CS_OK;
+}
+
+cs_status run_assign(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in k, int kq, int kk, int iters,
+                     uint64_t seed, int h_off, int h_tot, const int32_t* init_q, const int32_t* init_k, float* cq, float* ck,
+                     int32_t* lq, int32_t* lk, int32_t* perm_q, int32_t* offs_q, int32_t* perm_k,
+                     int32_t* offs_k, const AssignScratch& sc, __nv_bfloat16* qp_out,
+                     __nv_bfloat16* kp_out, cudaStream_t st) {
+  const int BH = B * H;
+  const XView xq = view(q, H), xk = view(k, H);
+  CS_CUDA(launch_init_sample(xq, xk, BH, N, d, kq, kk, seed, h_off, h_tot, init_q, init_k, cq, ck, st), "init_sample");
+  for (int it = 0; it < iters; ++it) {
+    const bool last = it == iters - 1;
+    // Step A: query-aware key-side partitioning
+    CS_CHECK(run_assign_step(B, H, N, d, k, kq, cq, kk, ck, lk, sc, st));
+    CS_CUDA(launch_csort(lk, BH, N, kk, perm_k, offs_k, sc.hist, st), "csort_k");
+    CS_CUDA(launch_seg_mean(xk, BH, N, d, kk, perm_k, offs_k, ck, last ? kp_out : nullptr, st), "seg_mean_k");
+    // Step B: key-aware query-side partitioning
+    CS_CHECK(run_assign_step(B, H, N, d, q, kk, ck, kq, cq, lq, sc, st));
+    CS_CUDA(launch_csort(lq, BH, N, kq, perm_q, offs_q, sc.hist, st), "csort_q");
+    CS_CUDA(launch_seg_mean(xq, BH, N, d, kq, perm_q, offs_q, cq, last ? qp_out : nullptr, st), "seg_mean_q");
+  }
+  return CS_OK;
+}
+
+cs_status run_attn(int B, int H, int N, int d, int kq, int kk, const int32_t* perm_q, const int32_t* offs_q,
+                   const int32_t* offs_k, const int32_t* n_keep, const int32_t* kept, float scale,
+                   cs_bf16_out o, const AttnScratch& sc, cudaStream_t st) {
+  const int BH = B * H;
+  CS_CUDA(launch_worklist(BH, kq, offs_q, sc.item_start, st), "worklist");
+  CUtensorMap tq, tk, tv;
+  CS_CHECK(make_map_2d(&tq, sc.qp, (uint64_t)BH * N, d, 128));
+  CS_CHECK(make_map_2d(&tk, sc.kp, (uint64_t)BH * N, d, 8));
+  CS_CHECK(make_map_2d(&tv, sc.vp, (uint64_t)BH * N, d, 8));
+  CS_CUDA(launch_bsa_fwd(&tq, &tk, &tv, BH, H, N, d, kq, kk, perm_q, offs_q, offs_k, n_keep, kept,
+                         sc.item_start, worklist_upper_bound(N, kq), scale,
+                         static_cast<__nv_bfloat16*>(o.ptr), o.sb, o.sh, o.sn, st),
+          "bsa_fwd");
+  return CS_OK;
+}
+
+}  // namespace
+
+// =================================================================== exported C ABI
+extern "C" {
+
+int cs_version(void) { return 100; }
+
+const char* cs_status_string(int s) {
+  switch (s) {
+    case CS_OK: return "CS_OK";
+    case CS_ERR_NULL: return "CS_ERR_NULL";
+    case CS_ERR_SHAPE: return "CS_ERR_SHAPE";
+    case CS_ERR_ARG: return "CS_ERR_ARG";
+    case CS_ERR_ALIGN: return "CS_ERR_ALIGN";
+    case CS_ERR_WORKSPACE: return "CS_ERR_WORKSPACE";
+    case CS_ERR_UNSUPPORTED: return "CS_ERR_UNSUPPORTED";
+    case CS_ERR_CUDA: return "CS_ERR_CUDA";
+  }
+  return "CS_ERR_UNKNOWN";
+}
+
+const char* cs_last_error(void) { return g_err; }
+
+size_t cs_workspace_bytes(int B, int H, int N, int d, int kq, int kk) {
+  if (B <= 0 || H <= 0 || N <= 0 || kq <= 0 || kk <= 0 || (d != 64 && d != 128)) return 0;
+  return need_layer(B * H, N, d, kq, kk);
+}
+
+cs_status check_heads(int H, int& h_off, int& h_tot) {
+  if (h_tot == 0) {
+    if (h_off != 0) return fail(CS_ERR_ARG, "head_offset must be 0 when heads_total is 0");
+    h_tot = H;
+  }
+  if (h_off < 0 || h_off + H > h_tot)
+    return fail(CS_ERR_ARG, "need 0 <= head_offset and head_offset + H <= heads_total (%d, %d, %d)", h_off, H, h_tot);
+  return CS_OK;
+}
+
+cs_status coclust_assign(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in k, int kq, int kk, int iters,
+                         uint64_t seed, int head_offset, int heads_total, const int32_t* init_q, const int32_t* init_k, float* cq, float* ck,
+                         int32_t* lq, int32_t* lk, int32_t* perm_q, int32_t* offs_q, int32_t* perm_k,
+                         int32_t* offs_k, void* ws, size_t ws_bytes, void* stream) {
+  g_err[0] = 0;
+  CS_CHECK(check_dims(B, H, N, d));
+  CS_CHECK(check_k(kq, N, "kq"));
+  CS_CHECK(check_k(kk, N, "kk"));
+  if (iters < 1) return fail(CS_ERR_ARG, "iters must be >= 1 (got %d)", iters);
+  CS_CHECK(check_heads(H, head_offset, heads_total));
+  CS_CHECK(check_bf16(q.ptr, q.sb, q.sh, q.sn, "q"));
+  CS_CHECK(check_bf16(k.ptr, k.sb, k.sh, k.sn, "k"));
+  NEED(cq, "cq"); NEED(ck, "ck"); NEED(lq, "lq"); NEED(lk, "lk");
+  NEED(perm_q, "perm_q"); NEED(offs_q, "offs_q"); NEED(perm_k, "perm_k"); NEED(offs_k, "offs_k");
+  const int BH = B * H;
+  CS_CHECK(check_ws(ws, ws_bytes, need_assign(BH, N, d, kq, kk)));
+  Carve c(ws);
+  AssignScratch sc = carve_assign(c, BH, N, d, kq, kk);
+  return run_assign(B, H, N, d, q, k, kq, kk, iters, seed, head_offset, heads_total, init_q, init_k, cq, ck, lq, lk, perm_q, offs_q,
+                    perm_k, offs_k, sc, nullptr, nullptr, static_cast<cudaStream_t>(stream));
+}
+
+cs_status coclust_assign_step(int B, int H, int N, int d, cs_bf16_in x, int ka, const float* c_anchor, int ks,
+                              const float* c_self, int32_t* labels, void* ws, size_t ws_bytes, void* stream) {
+  g_err[0] = 0;
+  CS_CHECK(check_dims(B, H, N, d));
+  if (ka < 1 || ka > kMaxClusters) return fail(CS_ERR_ARG, "ka must be in [1, %d] (got %d)", kMaxClusters, ka);
+  if (ks < 1 || ks > kMaxClusters) return fail(CS_ERR_ARG, "ks must be in [1, %d] (got %d)", kMaxClusters, ks);
+  CS_CHECK(check_bf16(x.ptr, x.sb, x.sh, x.sn, "x"));
+  NEED(c_anchor, "c_anchor"); NEED(c_self, "c_self"); NEED(labels, "labels");
+  const int BH = B * H;
+  CS_CHECK(check_ws(ws, ws_bytes, need_assign(BH, N, d, ka, ks)));
+  Carve c(ws);
+  AssignScratch sc = carve_assign(c, BH, N, d, ka, ks);
+  return run_assign_step(B, H, N, d, x, ka, c_anchor, ks, c_self, labels, sc, static_cast<cudaStream_t>(stream));
+}
+
+cs_status coclust_update_centroids(int B, int H, int N, int d, cs_bf16_in x, int k, const int32_t* perm,
+                                   const int32_t* offs, float* c_inout, void* x_perm, void* stream) {
+  g_err[0] = 0;
+  CS_CHECK(check_dims(B, H, N, d));
+  CS_CHECK(check_k(k, N, "k"));
+  CS_CHECK(check_bf16(x.ptr, x.sb, x.sh, x.sn, "x"));
+  NEED(perm, "perm"); NEED(offs, "offs"); NEED(c_inout, "c_inout");
+  if (x_perm && reinterpret_cast<uintptr_t>(x_perm) % 16) return fail(CS_ERR_ALIGN, "x_perm not 16-byte aligned");
+  CS_CUDA(launch_seg_mean(view(x, H), B * H, N, d, k, perm, offs, c_inout, static_cast<__nv_bfloat16*>(x_perm),
+                          static_cast<cudaStream_t>(stream)),
+          "seg_mean");
+  return CS_OK;
+}
+
+cs_status coclust_permute(int BH, int N, int k, const int32_t* labels, int32_t* perm, int32_t* offs, void* ws,
+                          size_t ws_bytes, void* stream) {
+  g_err[0] = 0;
+  if (BH <= 0 || N <= 0) return fail(CS_ERR_SHAPE, "BH, N must be positive");
+  if (N >= (1 << 24) || (long long)BH * N >= (1LL << 31)) return fail(CS_ERR_UNSUPPORTED, "too many tokens");
+  CS_CHECK(check_k(k, 1 << 30, "k"));
+  NEED(labels, "labels"); NEED(perm, "perm"); NEED(offs, "offs");
+  const size_t need = (size_t)BH * ((N + kSortTile - 1) / kSortTile) * k * 4 + 256;
+  CS_CHECK(check_ws(ws, ws_bytes, need));
+  Carve c(ws);
+  int32_t* hist = c.take<int32_t>((size_t)BH * ((N + kSortTile - 1) / kSortTile) * k);
+  CS_CUDA(launch_csort(labels, BH, N, k, perm, offs, hist, static_cast<cudaStream_t>(stream)), "csort");
+  return CS_OK;
+}
+
+cs_status block_select(int B, int H, int kq, int kk, int d, const float* cq, const float* ck,
+                       const int32_t* offs_q, const int32_t* offs_k, const float* budget, double tau,
+                       double theta, int rule, int32_t* n_keep, int32_t* kept, void* ws, size_t ws_bytes,
+                       void* stream) {
+  g_err[0] = 0;
+  if (B <= 0 || H <= 0) return fail(CS_ERR_SHAPE, "B, H must be positive");
+  if (d != 64 && d != 128) return fail(CS_ERR_SHAPE, "d must be 64 or 128 (got %d)", d);
+  CS_CHECK(check_k(kq, kMaxClusters, "kq"));
+  CS_CHECK(check_k(kk, kMaxClusters, "kk"));
+  if (!(tau > 0.0 && tau <= 1.0)) return fail(CS_ERR_ARG, "tau must be in (0, 1] (got %g)", tau);
+  if (!(theta > 0.0 && theta < 1.0)) return fail(CS_ERR_ARG, "theta must be in (0, 1) (got %g)", theta);
+  if (rule < 0 || rule > 2) return fail(CS_ERR_ARG, "unknown rule %d", rule);
+  NEED(cq, "cq"); NEED(ck, "ck"); NEED(offs_q, "offs_q"); NEED(offs_k, "offs_k"); NEED(budget, "budget");
+  NEED(n_keep, "n_keep"); NEED(kept, "kept");
+  const int BH = B * H;
+  CS_CHECK(check_ws(ws, ws_bytes, need_select(BH, kq, kk)));
+  Carve c(ws);
+  SelectScratch sc = carve_select(c, BH, kq, kk);
+  CS_CUDA(launch_block_select(BH, H, kq, kk, d, cq, ck, offs_q, offs_k, budget, tau, theta, rule, n_keep, kept,
+                              sc.order, sc.cnt, static_cast<cudaStream_t>(stream)),
+          "block_select");
+  return CS_OK;
+}
+
+cs_status block_sparse_attn(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in k, cs_bf16_in v, int kq, int kk,
+                            const int32_t* perm_q, const int32_t* offs_q, const int32_t* perm_k,
+                            const int32_t* offs_k, const int32_t* n_keep, const int32_t* kept, float scale,
+                            cs_bf16_out o, void* ws, size_t ws_bytes, void* stream) {
+  g_err[0] = 0;
+  CS_CHECK(check_dims(B, H, N, d));
+  CS_CHECK(check_k(kq, N, "kq"));
+  CS_CHECK(check_k(kk, N, "kk"));
+  CS_CHECK(check_bf16(q.ptr, q.sb, q.sh, q.sn, "q"));
+  CS_CHECK(check_bf16(k.ptr, k.sb, k.sh, k.sn, "k"));
+  CS_CHECK(check_bf16(v.ptr, v.sb, v.sh, v.sn, "v"));
+  CS_CHECK(check_bf16(o.ptr, o.sb, o.sh, o.sn, "o"));
+  if (!(scale > 0.f)) return fail(CS_ERR_ARG, "scale must be > 0 (got %g)", (double)scale);
+  NEED(perm_q, "perm_q"); NEED(offs_q, "offs_q"); NEED(perm_k, "perm_k"); NEED(offs_k, "offs_k");
+  NEED(n_keep, "n_keep"); NEED(kept, "kept");
+  const int BH = B * H;
+  CS_CHECK(check_ws(ws, ws_bytes, need_attn(BH, N, d, kq)));
+  Carve c(ws);
+  AttnScratch sc = carve_attn(c, BH, N, d, kq);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CS_CUDA(launch_permute_rows(view(q, H), BH, N, d, perm_q, sc.qp, st), "permute_q");
+  CS_CUDA(launch_permute_rows(view(k, H), BH, N, d, perm_k, sc.kp, st), "permute_k");
+  CS_CUDA(launch_permute_rows(view(v, H), BH, N, d, perm_k, sc.vp, st), "permute_v");
+  return run_attn(B, H, N, d, kq, kk, perm_q, offs_q, offs_k, n_keep, kept, scale, o, sc, st);
+}
+
+cs_status coclust_sparse_attention(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in k, cs_bf16_in v, int kq,
+                                   int kk, int iters, uint64_t seed, int head_offset, int heads_total,
+                                   const float* budget, double tau, double theta,
+                                   int rule, float scale, cs_bf16_out o, void* ws, size_t ws_bytes, void* stream) {
+  g_err[0] = 0;
+  CS_CHECK(check_dims(B, H, N, d));
+  CS_CHECK(check_k(kq, N, "kq"));
+  CS_CHECK(check_k(kk, N, "kk"));
+  if (iters < 1) return fail(CS_ERR_ARG, "iters must be >= 1 (got %d)", iters);
+  if (!(tau > 0.0 && tau <= 1.0)) return fail(CS_ERR_ARG, "tau must be in (0, 1] (got %g)", tau);
+  if (!(theta > 0.0 && theta < 1.0)) return fail(CS_ERR_ARG, "theta must be in (0, 1) (got %g)", theta);
+  if (rule < 0 || rule > 2) return fail(CS_ERR_ARG, "unknown rule %d", rule);
+  if (!(scale > 0.f)) return fail(CS_ERR_ARG, "scale must be > 0 (got %g)", (double)scale);
+  CS_CHECK(check_heads(H, head_offset, heads_total));
+  CS_CHECK(check_bf16(q.ptr, q.sb, q.sh, q.sn, "q"));
+  CS_CHECK(check_bf16(k.ptr, k.sb, k.sh, k.sn, "k"));
+  CS_CHECK(check_bf16(v.ptr, v.sb, v.sh, v.sn, "v"));
+  CS_CHECK(check_bf16(o.ptr, o.sb, o.sh, o.sn, "o"));
+  NEED(budget, "budget");
+  const int BH = B * H;
+  CS_CHECK(check_ws(ws, ws_bytes, need_layer(BH, N, d, kq, kk)));
+  Carve c(ws);
+  LayerState s = carve_state(c, BH, N, d, kq, kk);
+  AttnScratch at = carve_attn(c, BH, N, d, kq);
+  AssignScratch as = carve_assign(c, BH, N, d, kq, kk);
+  SelectScratch se = carve_select(c, BH, kq, kk);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CS_CHECK(run_assign(B, H, N, d, q, k, kq, kk, iters, seed, head_offset, heads_total, nullptr, nullptr, s.cq, s.ck, s.lq, s.lk, s.perm_q,
+                      s.offs_q, s.perm_k, s.offs_k, as, at.qp, at.kp, st));
+  CS_CUDA(launch_block_select(BH, H, kq, kk, d, s.cq, s.ck, s.offs_q, s.offs_k, budget, tau, theta, rule,
+                              s.n_keep, s.kept, se.order, se.cnt, st),
+          "block_select");
+  CS_CUDA(launch_permute_rows(view(v, H), BH, N, d, s.perm_k, at.vp, st), "permute_v");
+  return run_attn(B, H, N, d, kq, kk, s.perm_q, s.offs_q, s.offs_k, s.n_keep, s.kept, scale, o, at, st);
+}
+
+}  // extern "C"

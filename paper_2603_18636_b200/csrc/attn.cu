@@ -1,0 +1,355 @@
+// attn.cu — varlen block-sparse flash attention over co-clustered blocks for
+// sm_100a: "Dense attention is computed only over the top rho K_k blocks".
+//
+// One CTA = one work item (bh, query cluster a, pair of 128-row query tiles of a).  Q/K/V are the
+// cluster-sorted copies [BH, N, d] (bf16).  The kept key clusters of a are packed densely into
+// 128-key tiles made of 16 units of 8 consecutive sorted rows (one TMA box {64 cols, 8 rows} per
+// unit and d-half, landing on one 1024-B SWIZZLE_128B atom), so padding is < 8 rows per kept
+// cluster; rows of a unit past its cluster's end are masked to -inf in the softmax.
+//
+// Warp roles (320 threads):  warps 0-3 softmax/epilogue of Q tile 0 (TMEM lanes 0-127),
+// warps 4-7 the same for Q tile 1, warp 8 TMA producer, warp 9 TMEM allocator + MMA issuer.
+// TMEM (512 cols): S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512); P (bf16x2) overwrites the
+// first 64 columns of its S buffer and feeds the PV MMA from TMEM (A operand), V from SMEM
+// (MN-major).  MMA issue order per KV tile j:  PV0(j), QK0(j+1), PV1(j), QK1(j+1), so the softmax
+// of one tile overlaps the MMAs of the other (FA4-style ping-pong).  Online softmax in the exp2
+// domain with lazy rescaling (only when the running max grows by > 8, i.e. a factor 256).
+// The inverse permutation is fused into the epilogue: row r of the tile is stored as 16-byte
+// vectors to O[b, h, perm_q[p], :] in original token order.
+#include "kernels.cuh"
+
+namespace cs {
+namespace attn {
+
+constexpr int BM = 128, BN = 128, UNIT = 8, UPT = BN / UNIT, NST = 2;
+constexpr int NTHREADS = 320;
+constexpr int WARP_PRODUCER = 8, WARP_MMA = 9;
+constexpr float kRescaleThresh = 8.0f;
+
+template <int D>
+struct Smem {
+  static constexpr int HALVES = D / 64;
+  static constexpr int QT = BM * D * 2;   // bytes per Q tile
+  static constexpr int KT = BN * D * 2;   // bytes per K (or V) tile
+  static constexpr int HALF_Q = BM * 128;  // bytes per 64-col half of a Q tile
+  static constexpr int HALF_K = BN * 128;
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_K = OFF_Q + 2 * QT;
+  static constexpr int OFF_V = OFF_K + NST * KT;
+  static constexpr int OFF_BAR = OFF_V + NST * KT;
+  // barriers: q_full, kv_full[NST], kv_empty[NST], s_full[2], p_full[2], o_full  (8 B each)
+  static constexpr int NBAR = 1 + 2 * NST + 2 + 2 + 1;
+  static constexpr int OFF_VMASK = OFF_BAR + 8 * 16;
+  static constexpr int OFF_MISC = OFF_VMASK + NST * UPT;  // tmem slot, U, nt
+  static constexpr int OFF_KSTART = OFF_MISC + 64;
+  static constexpr int OFF_KLEN = OFF_KSTART + kMaxClusters * 4;
+  static constexpr int OFF_UCUM = OFF_KLEN + kMaxClusters * 4;
+  static constexpr int BYTES = OFF_UCUM + (kMaxClusters + 1) * 4;
+  static constexpr int ALLOC = BYTES + 1024;  // room to align the base to 1024
+};
+
+template <int D>
+__global__ void __launch_bounds__(NTHREADS, 1)
+    k_bsa_fwd(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+              const __grid_constant__ CUtensorMap tm_v, int H, int N, int kq, int kk,
+              const int32_t* __restrict__ perm_q, const int32_t* __restrict__ offs_q,
+              const int32_t* __restrict__ offs_k, const int32_t* __restrict__ n_keep,
+              const int32_t* __restrict__ kept, const int32_t* __restrict__ item_start,
+              float scale_log2, __nv_bfloat16* __restrict__ out, long long osb, long long osh,
+              long long osn) {
+  using L = Smem<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::OFF_BAR);
+  uint64_t* q_full = bars;
+  uint64_t* kv_full = bars + 1;
+  uint64_t* kv_empty = bars + 1 + NST;
+  uint64_t* s_full = bars + 1 + 2 * NST;
+  uint64_t* p_full = s_full + 2;
+  uint64_t* o_full = p_full + 2;
+  uint8_t* vmask = sm + L::OFF_VMASK;
+  int* misc = reinterpret_cast<int*>(sm + L::OFF_MISC);
+  int* kstart = reinterpret_cast<int*>(sm + L::OFF_KSTART);
+  int* klen = reinterpret_cast<int*>(sm + L::OFF_KLEN);
+  int* ucum = reinterpret_cast<int*>(sm + L::OFF_UCUM);
+
+  const int bh = blockIdx.y;
+  const int item = blockIdx.x;
+  const int32_t* ist = item_start + (size_t)bh * (kq + 1);
+  if (item >= ist[kq]) return;  // uniform across the CTA
+  // query cluster a: largest a with ist[a] <= item
+  int lo = 0, hi = kq - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (ist[mid] <= item) lo = mid; else hi = mid - 1;
+  }
+  const int a = lo;
+  const int pair = item - ist[a];
+  const int qbeg = offs_q[(size_t)bh * (kq + 1) + a];
+  const int qlen = offs_q[(size_t)bh * (kq + 1) + a + 1] - qbeg;
+  const int t0 = 2 * pair;
+  const bool has1 = (t0 + 1) * BM < qlen;
+  const int warp = warp_id(), lane = lane_id();
+
+  // ---- setup: barriers (thread 0), TMEM (warp 9), unit table (warp 8)
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    for (int s = 0; s < NST; ++s) { mbar_init(kv_full + s, 1); mbar_init(kv_empty + s, 1); }
+    for (int t = 0; t < 2; ++t) { mbar_init(s_full + t, 1); mbar_init(p_full + t, 128); }
+    mbar_init(o_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == WARP_MMA) tmem_alloc(reinterpret_cast<uint32_t*>(misc), 512);
+  if (warp == WARP_PRODUCER) {
+    tma_prefetch_desc(&tm_q); tma_prefetch_desc(&tm_k); tma_prefetch_desc(&tm_v);
+    const int n = n_keep[bh];
+    const int32_t* kl = kept + ((size_t)bh * kq + a) * kk;
+    const int32_t* ok = offs_k + (size_t)bh * (kk + 1);
+    int carry = 0;
+    for (int i0 = 0; i0 < n; i0 += 32) {
+      const int i = i0 + lane;
+      int nu = 0;
+      if (i < n) {
+        const int c = kl[i];
+        const int st = ok[c];
+        const int len = ok[c + 1] - st;
+        kstart[i] = st; klen[i] = len;
+        nu = (len + UNIT - 1) / UNIT;
+      }
+      int x = nu;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) { int y = __shfl_up_sync(0xffffffffu, x, o); if (lane >= o) x += y; }
+      if (i < n) ucum[i] = carry + x - nu;
+      carry += __shfl_sync(0xffffffffu, x, 31);
+    }
+    if (lane == 0) { ucum[n] = carry; misc[1] = carry; misc[2] = n; }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = static_cast<uint32_t>(misc[0]);
+  const int U = misc[1];
+  const int nkeep = misc[2];
+  const int nt = (U + UPT - 1) / UPT;
+
+  if (warp == WARP_PRODUCER) {
+    // ================= TMA producer =================
+    if (lane == 0) {
+      const int ntq = has1 ? 2 : 1;
+      mbar_arrive_expect_tx(q_full, ntq * L::QT);
+      for (int tq = 0; tq < ntq; ++tq)
+        for (int hf = 0; hf < L::HALVES; ++hf)
+          tma_load_2d(sm + L::OFF_Q + tq * L::QT + hf * L::HALF_Q, &tm_q, hf * 64,
+                      bh * N + qbeg + (t0 + tq) * BM, q_full);
+    }
+    for (int j = 0; j < nt; ++j) {
+      const int stage = j % NST;
+      mbar_wait(kv_empty + stage, ((j / NST) & 1) ^ 1);
+      int row = bh * N + kstart[0], valid = 0;
+      if (lane < UPT) {
+        const int g = j * UPT + lane;
+        if (g < U) {
+          int l2 = 0, h2 = nkeep - 1;
+          while (l2 < h2) {
+            const int mid = (l2 + h2 + 1) >> 1;
+            if (ucum[mid] <= g) l2 = mid; else h2 = mid - 1;
+          }
+          const int u = g - ucum[l2];
+          row = bh * N + kstart[l2] + u * UNIT;
+          valid = min(UNIT, klen[l2] - u * UNIT);
+        }
+        vmask[stage * UPT + lane] = (uint8_t)valid;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive_expect_tx(kv_full + stage, 2 * L::KT);
+      __syncwarp();
+      if (lane < UPT) {
+        for (int hf = 0; hf < L::HALVES; ++hf) {
+          tma_load_2d(sm + L::OFF_K + stage * L::KT + hf * L::HALF_K + lane * 1024, &tm_k, hf * 64,
+                      row, kv_full + stage);
+          tma_load_2d(sm + L::OFF_V + stage * L::KT + hf * L::HALF_K + lane * 1024, &tm_v, hf * 64,
+                      row, kv_full + stage);
+        }
+      }
+    }
+  } else if (warp == WARP_MMA) {
+    // ================= MMA issuer (one thread) =================
+    if (lane == 0) {
+      constexpr uint32_t idesc_qk = idesc_bf16(BM, BN, 0, 0);
+      constexpr uint32_t idesc_pv = idesc_bf16(BM, D, 0, 1);
+      const uint32_t sQ = smem_u32(sm + L::OFF_Q), sK = smem_u32(sm + L::OFF_K),
+                     sV = smem_u32(sm + L::OFF_V);
+      auto issue_qk = [&](int tq, int stage) {
+        const uint32_t d_tmem = tmem + tq * 128;
+#pragma unroll
+        for (int kk2 = 0; kk2 < D / 16; ++kk2) {
+          const uint32_t off = (kk2 >> 2) * L::HALF_Q + (kk2 & 3) * 32;
+          const uint32_t offk = (kk2 >> 2) * L::HALF_K + (kk2 & 3) * 32;
+          const uint64_t ad = smem_desc_sw128(sQ + tq * L::QT + off, 16, 1024);
+          const uint64_t bd = smem_desc_sw128(sK + stage * L::KT + offk, 16, 1024);
+          mma_ss(d_tmem, ad, bd, idesc_qk, kk2 > 0);
+        }
+      };
+      auto issue_pv = [&](int tq, int stage, bool acc) {
+        const uint32_t d_tmem = tmem + 256 + tq * 128;
+        const uint32_t p_tmem = tmem + tq * 128;
+#pragma unroll
+        for (int kk2 = 0; kk2 < BN / 16; ++kk2) {
+          const uint64_t bd = smem_desc_sw128(sV + stage * L::KT + kk2 * 2048, L::HALF_K, 1024);
+          mma_ts(d_tmem, p_tmem + kk2 * 8, bd, idesc_pv, (acc || kk2 > 0) ? 1u : 0u);
+        }
+      };
+      mbar_wait(q_full, 0);
+      mbar_wait(kv_full, 0);
+      tc_fence_after();
+      issue_qk(0, 0);
+      mma_commit(s_full + 0);
+      if (has1) { issue_qk(1, 0); mma_commit(s_full + 1); }
+      for (int j = 0; j < nt; ++j) {
+        const int stage = j % NST, stage1 = (j + 1) % NST;
+        const bool more = j + 1 < nt;
+        mbar_wait(p_full + 0, j & 1);
+        tc_fence_after();
+        issue_pv(0, stage, j > 0);
+        if (more) {
+          mbar_wait(kv_full + stage1, ((j + 1) / NST) & 1);
+          tc_fence_after();
+          issue_qk(0, stage1);
+          mma_commit(s_full + 0);
+        }
+        if (has1) {
+          mbar_wait(p_full + 1, j & 1);
+          tc_fence_after();
+          issue_pv(1, stage, j > 0);
+        }
+        mma_commit(kv_empty + stage);
+        if (has1 && more) { issue_qk(1, stage1); mma_commit(s_full + 1); }
+      }
+      mma_commit(o_full);
+    }
+    __syncwarp();
+  } else {
+    // ================= softmax / epilogue (warps 0-7) =================
+    const int tq = warp >> 2;
+    if (tq == 0 || has1) {
+      const int quad = warp & 3;
+      const int r = quad * 32 + lane;  // row of the Q tile == TMEM lane
+      const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+      const uint32_t s_tm = tmem + lane_off + tq * 128;
+      const uint32_t o_tm = tmem + lane_off + 256 + tq * 128;
+      float m = -INFINITY, l = 0.f;
+      for (int j = 0; j < nt; ++j) {
+        const int stage = j % NST;
+        mbar_wait(s_full + tq, j & 1);
+        tc_fence_after();
+        uint32_t su[BN];
+#pragma unroll
+        for (int c = 0; c < BN / 32; ++c) tmem_ld32(s_tm + c * 32, su + c * 32);
+        tmem_wait_ld();
+        mbar_wait(kv_full + stage, (j / NST) & 1);
+        const uint4 vw = *reinterpret_cast<const uint4*>(vmask + stage * UPT);
+        float mx = -INFINITY;
+#pragma unroll
+        for (int c = 0; c < BN; ++c) {
+          const uint32_t word = (c < 32) ? vw.x : (c < 64) ? vw.y : (c < 96) ? vw.z : vw.w;
+          const uint32_t vcnt = (word >> (8 * ((c >> 3) & 3))) & 0xffu;
+          const float v = ((uint32_t)(c & 7) < vcnt) ? __uint_as_float(su[c]) * scale_log2 : -INFINITY;
+          su[c] = __float_as_uint(v);
+          mx = fmaxf(mx, v);
+        }
+        float alpha = 1.f;
+        if (j == 0) {
+          m = mx;
+        } else if (mx > m + kRescaleThresh) {
+          alpha = ex2(m - mx);
+          l *= alpha;
+          m = mx;
+        }
+        float rs = 0.f;
+#pragma unroll
+        for (int c = 0; c < BN; c += 2) {
+          const float p0 = ex2(__uint_as_float(su[c]) - m), p1 = ex2(__uint_as_float(su[c + 1]) - m);
+          rs += p0 + p1;
+          su[c >> 1] = pack_bf16x2(p0, p1);
+        }
+        l += rs;
+        tmem_st32(s_tm, su);
+        tmem_st32(s_tm + 32, su + 32);
+        if (alpha != 1.f) {  // lazy O rescale; PV(j) is not issued before p_full(j)
+#pragma unroll 1
+          for (int c = 0; c < D / 32; ++c) {
+            uint32_t ov[32];
+            tmem_ld32(o_tm + c * 32, ov);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
+            tmem_st32(o_tm + c * 32, ov);
+          }
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(p_full + tq);
+      }
+      // ---- epilogue: O / l -> bf16, scattered to original token order
+      mbar_wait(o_full, 0);
+      tc_fence_after();
+      const int prow = (t0 + tq) * BM + r;
+      const bool row_ok = prow < qlen;
+      const float inv_l = 1.f / l;
+      const int tok = row_ok ? perm_q[(size_t)bh * N + qbeg + prow] : 0;
+      const int b = bh / H, h = bh % H;
+      __nv_bfloat16* dst = out + (long long)b * osb + (long long)h * osh + (long long)tok * osn;
+#pragma unroll
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t ov[32];
+        tmem_ld32(o_tm + c * 32, ov);
+        tmem_wait_ld();
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          pk[i] = pack_bf16x2(__uint_as_float(ov[2 * i]) * inv_l, __uint_as_float(ov[2 * i + 1]) * inv_l);
+        if (row_ok) {
+          uint4* d4 = reinterpret_cast<uint4*>(dst + c * 32);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) d4[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == WARP_MMA) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+}  // namespace attn
+
+cudaError_t launch_bsa_fwd(const CUtensorMap* tm_q, const CUtensorMap* tm_k, const CUtensorMap* tm_v,
+                           int BH, int H, int N, int d, int kq, int kk, const int32_t* perm_q,
+                           const int32_t* offs_q, const int32_t* offs_k, const int32_t* n_keep,
+                           const int32_t* kept, const int32_t* item_start, int items_ub,
+                           float scale, __nv_bfloat16* o, long long osb, long long osh,
+                           long long osn, cudaStream_t st) {
+  const float scale_log2 = scale * 1.4426950408889634f;
+  dim3 grid(items_ub, BH);
+  if (d == 128) {
+    auto kfn = attn::k_bsa_fwd<128>;
+    const int smem = attn::Smem<128>::ALLOC;
+    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    kfn<<<grid, attn::NTHREADS, smem, st>>>(*tm_q, *tm_k, *tm_v, H, N, kq, kk, perm_q, offs_q, offs_k,
+                                           n_keep, kept, item_start, scale_log2, o, osb, osh, osn);
+  } else {
+    auto kfn = attn::k_bsa_fwd<64>;
+    const int smem = attn::Smem<64>::ALLOC;
+    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    kfn<<<grid, attn::NTHREADS, smem, st>>>(*tm_q, *tm_k, *tm_v, H, N, kq, kk, perm_q, offs_q, offs_k,
+                                           n_keep, kept, item_start, scale_log2, o, osb, osh, osn);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace cs

@@ -1,0 +1,419 @@
+// cluster.cu — co-clustering support kernels for Alg. 1 on sm_100a:
+//   k_init_sample   : Sample(X, K) (R4) + C^(0) = X[idx]
+//   k_gamma         : Gamma = C_a^T C_a (fp64)               } anchor prep for the reduced-form
+//   k_anchor_w      : W_j = Gamma c_j / ||c_j C_a^T|| -> bf16 } assignment (a2)
+//                     hi/lo split
+//   k_seg_mean      : C_j = mean of the members of cluster j, optional permuted copy
+//   k_csort_*       : stable counting sort labels -> perm, offs (implied by P:1266)
+//   k_permute_rows  : x_perm[p] = x[perm[p]]
+#include "kernels.cuh"
+
+namespace cs {
+
+// ---------------------------------------------------------------------------------------------
+// block-wide exclusive scan (int), blockDim.x multiple of 32, <= 1024
+// ---------------------------------------------------------------------------------------------
+__device__ int block_exclusive_scan(int v, int* total, int* sbuf /*[32]*/) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sbuf[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int s = lane < nw ? sbuf[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    sbuf[lane] = s;  // inclusive warp totals
+  }
+  __syncthreads();
+  int base = w > 0 ? sbuf[w - 1] : 0;
+  if (total) *total = sbuf[nw - 1];
+  int r = base + x - v;
+  __syncthreads();
+  return r;
+}
+
+// ---------------------------------------------------------------------------------------------
+// a1: init sampling.  grid (BH, 2 sides), block 256, dyn smem = bitmap words + idx[K]
+// ---------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_init_sample(XView q, XView k, int N, int d, int kq, int kk,
+                                                     unsigned long long seed, int h_off, int h_tot,
+                                                     const int32_t* __restrict__ init_q,
+                                                     const int32_t* __restrict__ init_k,
+                                                     float* __restrict__ cq, float* __restrict__ ck) {
+  extern __shared__ uint32_t sm_bits[];
+  __shared__ int sbuf[32];
+  const int bh = blockIdx.x, side = blockIdx.y;
+  const int K = side ? kk : kq;
+  const int32_t* init = side ? init_k : init_q;
+  const XView X = side ? k : q;
+  float* C = (side ? ck : cq) + (size_t)bh * K * d;
+  const int nwords = (N + 31) >> 5;
+  int* idx = reinterpret_cast<int*>(sm_bits + nwords);
+  if (init) {
+    for (int j = threadIdx.x; j < K; j += blockDim.x) idx[j] = init[(size_t)bh * K + j];
+  } else {
+    for (int w = threadIdx.x; w < nwords; w += blockDim.x) sm_bits[w] = 0u;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      // R4: splitmix64 stream, Floyd's algorithm.
+      const long long key = (long long)(bh / X.H) * h_tot + h_off + bh % X.H;  // b*Ht + hg
+      unsigned long long state = seed ^ ((unsigned long long)(key * 2 + side) * 0x9E3779B97F4A7C15ull);
+      for (int j = N - K; j < N; ++j) {
+        state += 0x9E3779B97F4A7C15ull;
+        unsigned long long z = state;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        z ^= z >> 31;
+        const int t = (int)(z % (unsigned long long)(j + 1));
+        const int pick = ((sm_bits[t >> 5] >> (t & 31)) & 1u) ? j : t;
+        sm_bits[pick >> 5] |= 1u << (pick & 31);
+      }
+    }
+    __syncthreads();
+    // ascending compaction of the bitmap: each thread owns a contiguous word range
+    const int per = (nwords + blockDim.x - 1) / blockDim.x;
+    const int w0 = threadIdx.x * per, w1 = min(nwords, w0 + per);
+    int cnt = 0;
+    for (int w = w0; w < w1; ++w) cnt += __popc(sm_bits[w]);
+    int pos = block_exclusive_scan(cnt, nullptr, sbuf);
+    for (int w = w0; w < w1; ++w) {
+      uint32_t m = sm_bits[w];
+      while (m) {
+        int b = __ffs(m) - 1;
+        m &= m - 1;
+        idx[pos++] = (w << 5) + b;
+      }
+    }
+  }
+  __syncthreads();
+  // C^(0)[j] = X[idx[j]]  (bf16 -> fp32)
+  const int b = bh / X.H, h = bh % X.H;
+  for (int e = threadIdx.x; e < K * d; e += blockDim.x) {
+    const int j = e / d, c = e % d;
+    C[e] = __bfloat162float(X.row(b, h, idx[j])[c]);
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// a2: Gamma = C_a^T C_a (fp64).  grid (BH, d/16), block 256: rows e in [16 by, 16 by + 16)
+// ---------------------------------------------------------------------------------------------
+template <int D>
+__global__ void __launch_bounds__(256) k_gamma(const float* __restrict__ ca, int ka,
+                                               double* __restrict__ gamma) {
+  constexpr int ROWS = 16, CH = 32, EPT = ROWS * D / 256;
+  __shared__ double sa[CH][D];
+  const int bh = blockIdx.x, e0 = blockIdx.y * ROWS;
+  const float* A = ca + (size_t)bh * ka * D;
+  const int t = threadIdx.x;
+  const int flat = t * EPT;
+  const int e = e0 + flat / D, f0 = flat % D;
+  double acc[EPT];
+#pragma unroll
+  for (int i = 0; i < EPT; ++i) acc[i] = 0.0;
+  for (int a0 = 0; a0 < ka; a0 += CH) {
+    const int n = min(CH, ka - a0);
+    __syncthreads();
+    for (int i = t; i < CH * D; i += 256) {
+      const int r = i / D, c = i % D;
+      sa[r][c] = r < n ? (double)A[(size_t)(a0 + r) * D + c] : 0.0;
+    }
+    __syncthreads();
+    for (int r = 0; r < n; ++r) {
+      const double ae = sa[r][e];
+#pragma unroll
+      for (int i = 0; i < EPT; ++i) acc[i] = fma(ae, sa[r][f0 + i], acc[i]);
+    }
+  }
+  double* G = gamma + (size_t)bh * D * D + (size_t)e * D + f0;
+#pragma unroll
+  for (int i = 0; i < EPT; ++i) G[i] = acc[i];
+}
+
+// ---------------------------------------------------------------------------------------------
+// a2: W_j = Gamma c_j / ||c_j C_a^T||  ->  Wsplit[bh][j] = [bf16(W) | bf16(W - bf16(W))]
+// grid (ks_pad / 8, BH), block 128.  Rows j >= ks are written as zeros (padding).
+// ---------------------------------------------------------------------------------------------
+template <int D>
+__global__ void __launch_bounds__(128) k_anchor_w(const float* __restrict__ ca, int ka,
+                                                  const float* __restrict__ cs_, int ks, int ks_pad,
+                                                  const double* __restrict__ gamma,
+                                                  __nv_bfloat16* __restrict__ wsplit) {
+  constexpr int J = 8;
+  __shared__ double sc[J][D];
+  __shared__ double red[J][4];
+  __shared__ double inv_norm[J];
+  const int bh = blockIdx.y, j0 = blockIdx.x * J, t = threadIdx.x;
+  const float* A = ca + (size_t)bh * ka * D;
+  const float* S = cs_ + (size_t)bh * ks * D;
+  for (int i = t; i < J * D; i += 128) {
+    const int r = i / D, c = i % D;
+    sc[r][c] = (j0 + r < ks) ? (double)S[(size_t)(j0 + r) * D + c] : 0.0;
+  }
+  __syncthreads();
+  // ||u_j||^2 with u_j[a] = c_j . C_a[a]
+  double sq[J];
+#pragma unroll
+  for (int r = 0; r < J; ++r) sq[r] = 0.0;
+  for (int a = t; a < ka; a += 128) {
+    const float* row = A + (size_t)a * D;
+    double u[J];
+#pragma unroll
+    for (int r = 0; r < J; ++r) u[r] = 0.0;
+    for (int c = 0; c < D; ++c) {
+      const double v = (double)row[c];
+#pragma unroll
+      for (int r = 0; r < J; ++r) u[r] = fma(v, sc[r][c], u[r]);
+    }
+#pragma unroll
+    for (int r = 0; r < J; ++r) sq[r] = fma(u[r], u[r], sq[r]);
+  }
+#pragma unroll
+  for (int r = 0; r < J; ++r) {
+    double v = sq[r];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((t & 31) == 0) red[r][t >> 5] = v;
+  }
+  __syncthreads();
+  if (t < J) {
+    const double n2 = red[t][0] + red[t][1] + red[t][2] + red[t][3];
+    inv_norm[t] = n2 > 0.0 ? 1.0 / sqrt(n2) : 0.0;  // ||Pbar_j|| = 0 -> W_j = 0
+  }
+  __syncthreads();
+  if (t < D) {
+    const double* G = gamma + (size_t)bh * D * D + (size_t)t * D;
+    double w[J];
+#pragma unroll
+    for (int r = 0; r < J; ++r) w[r] = 0.0;
+    for (int f = 0; f < D; ++f) {
+      const double g = G[f];
+#pragma unroll
+      for (int r = 0; r < J; ++r) w[r] = fma(g, sc[r][f], w[r]);
+    }
+#pragma unroll
+    for (int r = 0; r < J; ++r) {
+      const int j = j0 + r;
+      if (j >= ks_pad) break;
+      __nv_bfloat16* out = wsplit + ((size_t)bh * ks_pad + j) * (2 * D);
+      if (j < ks) {
+        const double wv = w[r] * inv_norm[r];
+        const __nv_bfloat16 hi = __double2bfloat16(wv);
+        const __nv_bfloat16 lo = __double2bfloat16(wv - (double)__bfloat162float(hi));
+        out[t] = hi;
+        out[D + t] = lo;
+      } else {
+        out[t] = __float2bfloat16(0.f);
+        out[D + t] = __float2bfloat16(0.f);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// a5/a7: centroid update.  grid (K, BH), block 256 (8 warps); warp w sums a contiguous chunk of
+// the cluster's sorted positions; fixed order -> deterministic.  Empty cluster: untouched (R5).
+// ---------------------------------------------------------------------------------------------
+template <int D>
+__global__ void __launch_bounds__(256) k_seg_mean(XView x, int N, int K,
+                                                  const int32_t* __restrict__ perm,
+                                                  const int32_t* __restrict__ offs,
+                                                  float* __restrict__ C,
+                                                  __nv_bfloat16* __restrict__ xperm) {
+  constexpr int VEC = D / 32;  // bf16 per lane (4 or 2)
+  constexpr int NW = 8, U = 8;
+  __shared__ float part[NW][D];
+  const int bh = blockIdx.y, j = blockIdx.x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int32_t* of = offs + (size_t)bh * (K + 1);
+  const int beg = of[j], end = of[j + 1], cnt = end - beg;
+  if (cnt == 0) return;
+  const int b = bh / x.H, h = bh % x.H;
+  const int chunk = (cnt + NW - 1) / NW;
+  const int p0 = beg + w * chunk, p1 = min(end, p0 + chunk);
+  const int32_t* pm = perm + (size_t)bh * N;
+  float acc[VEC];
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) acc[i] = 0.f;
+  using VT = typename std::conditional<VEC == 4, uint2, uint32_t>::type;
+  for (int p = p0; p < p1; p += U) {
+    VT v[U];
+    int tok[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) tok[u] = (p + u < p1) ? pm[p + u] : -1;
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (tok[u] >= 0) v[u] = *reinterpret_cast<const VT*>(x.row(b, h, tok[u]) + lane * VEC);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (tok[u] < 0) break;
+      const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&v[u]);
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) acc[i] += __bfloat162float(e[i]);
+      if (xperm)
+        *reinterpret_cast<VT*>(xperm + ((size_t)bh * N + p + u) * D + lane * VEC) = v[u];
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) part[w][lane * VEC + i] = acc[i];
+  __syncthreads();
+  if (threadIdx.x < D) {
+    float s = 0.f;
+#pragma unroll
+    for (int ww = 0; ww < NW; ++ww) s += part[ww][threadIdx.x];
+    C[((size_t)bh * K + j) * D + threadIdx.x] = s / (float)cnt;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// a4/a7: stable counting sort.  Tiles of kSortTile tokens.
+// ---------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_csort_hist(const int32_t* __restrict__ lab, int N, int K,
+                                                    int ntiles, int32_t* __restrict__ hist) {
+  extern __shared__ int sh_hist[];
+  const int bh = blockIdx.y, t = blockIdx.x;
+  for (int c = threadIdx.x; c < K; c += blockDim.x) sh_hist[c] = 0;
+  __syncthreads();
+  const int i0 = t * kSortTile, i1 = min(N, i0 + kSortTile);
+  const int32_t* L = lab + (size_t)bh * N;
+  for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) atomicAdd(&sh_hist[L[i]], 1);
+  __syncthreads();
+  int32_t* H = hist + ((size_t)bh * ntiles + t) * K;
+  for (int c = threadIdx.x; c < K; c += blockDim.x) H[c] = sh_hist[c];
+}
+
+// grid BH, block 1024 (K <= 1024): hist (counts) -> per-tile bases in place; offs.
+__global__ void __launch_bounds__(1024) k_csort_scan(int N, int K, int ntiles,
+                                                     int32_t* __restrict__ hist,
+                                                     int32_t* __restrict__ offs) {
+  __shared__ int sbuf[32];
+  const int bh = blockIdx.x, c = threadIdx.x;
+  int32_t* H = hist + (size_t)bh * ntiles * K;
+  int tot = 0;
+  if (c < K)
+    for (int t = 0; t < ntiles; ++t) tot += H[(size_t)t * K + c];
+  int start = block_exclusive_scan(tot, nullptr, sbuf);
+  if (c < K) {
+    offs[(size_t)bh * (K + 1) + c] = start;
+    int base = start;
+    for (int t = 0; t < ntiles; ++t) {
+      const int h = H[(size_t)t * K + c];
+      H[(size_t)t * K + c] = base;
+      base += h;
+    }
+  }
+  if (c == 0) offs[(size_t)bh * (K + 1) + K] = N;
+}
+
+// grid (ceil(ntiles/4), BH), block 128: one warp per tile, in token order.
+__global__ void __launch_bounds__(128) k_csort_scatter(const int32_t* __restrict__ lab, int N, int K,
+                                                       int ntiles, const int32_t* __restrict__ base,
+                                                       int32_t* __restrict__ perm) {
+  extern __shared__ int sh_cnt[];  // [4][K]
+  const int bh = blockIdx.y, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t = blockIdx.x * 4 + w;
+  if (t >= ntiles) return;
+  int* cnt = sh_cnt + w * K;
+  const int32_t* B0 = base + ((size_t)bh * ntiles + t) * K;
+  for (int c = lane; c < K; c += 32) cnt[c] = B0[c];
+  __syncwarp();
+  const int32_t* L = lab + (size_t)bh * N;
+  int32_t* P = perm + (size_t)bh * N;
+  const int i0 = t * kSortTile, i1 = min(N, i0 + kSortTile);
+  const unsigned lt = (1u << lane) - 1u;
+  for (int i = i0; i < i1; i += 32) {
+    const int me = i + lane;
+    const bool valid = me < i1;
+    const int l = valid ? L[me] : -1 - lane;  // unique dummy keys for the tail
+    const unsigned peers = __match_any_sync(0xffffffffu, l);
+    const int rank = __popc(peers & lt);
+    const int basep = valid ? cnt[l] : 0;
+    __syncwarp();
+    if (valid) {
+      P[basep + rank] = me;
+      if (rank == 0) cnt[l] = basep + __popc(peers);
+    }
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// x_perm[bh][p][:] = x[b,h,perm[bh][p],:].  grid (ceil(N/16), BH), block 256 (16 rows / block)
+// ---------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_permute_rows(XView x, int N, int d,
+                                                      const int32_t* __restrict__ perm,
+                                                      __nv_bfloat16* __restrict__ xp) {
+  const int bh = blockIdx.y;
+  const int lanes_per_row = d / 8;  // 16-byte chunks per row
+  const int rows_per_block = 256 / lanes_per_row;
+  const int r = threadIdx.x / lanes_per_row, c = threadIdx.x % lanes_per_row;
+  const int p = blockIdx.x * rows_per_block + r;
+  if (p >= N) return;
+  const int tok = perm[(size_t)bh * N + p];
+  const int b = bh / x.H, h = bh % x.H;
+  const uint4 v = *reinterpret_cast<const uint4*>(x.row(b, h, tok) + c * 8);
+  *reinterpret_cast<uint4*>(xp + ((size_t)bh * N + p) * d + c * 8) = v;
+}
+
+// ---------------------------------------------------------------------------------------------
+// host-side launchers
+// ---------------------------------------------------------------------------------------------
+cudaError_t launch_init_sample(XView q, XView k, int BH, int N, int d, int kq, int kk,
+                               unsigned long long seed, int h_off, int h_tot, const int32_t* init_q,
+                               const int32_t* init_k, float* cq, float* ck, cudaStream_t st) {
+  const size_t smem = (size_t)((N + 31) / 32) * 4 + (size_t)max(kq, kk) * 4;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k_init_sample, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  k_init_sample<<<dim3(BH, 2), 256, smem, st>>>(q, k, N, d, kq, kk, seed, h_off, h_tot, init_q, init_k,
+                                                cq, ck);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_anchor_prep(const float* ca, int ka, const float* cself, int ks, int ks_pad,
+                               int BH, int d, double* gamma, __nv_bfloat16* wsplit, cudaStream_t st) {
+  if (d == 128) {
+    k_gamma<128><<<dim3(BH, 128 / 16), 256, 0, st>>>(ca, ka, gamma);
+    k_anchor_w<128><<<dim3((ks_pad + 7) / 8, BH), 128, 0, st>>>(ca, ka, cself, ks, ks_pad, gamma, wsplit);
+  } else {
+    k_gamma<64><<<dim3(BH, 64 / 16), 256, 0, st>>>(ca, ka, gamma);
+    k_anchor_w<64><<<dim3((ks_pad + 7) / 8, BH), 128, 0, st>>>(ca, ka, cself, ks, ks_pad, gamma, wsplit);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_seg_mean(XView x, int BH, int N, int d, int K, const int32_t* perm,
+                            const int32_t* offs, float* C, __nv_bfloat16* xperm, cudaStream_t st) {
+  if (d == 128)
+    k_seg_mean<128><<<dim3(K, BH), 256, 0, st>>>(x, N, K, perm, offs, C, xperm);
+  else
+    k_seg_mean<64><<<dim3(K, BH), 256, 0, st>>>(x, N, K, perm, offs, C, xperm);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_csort(const int32_t* lab, int BH, int N, int K, int32_t* perm, int32_t* offs,
+                         int32_t* hist, cudaStream_t st) {
+  const int ntiles = (N + kSortTile - 1) / kSortTile;
+  k_csort_hist<<<dim3(ntiles, BH), 256, K * sizeof(int), st>>>(lab, N, K, ntiles, hist);
+  k_csort_scan<<<BH, 1024, 0, st>>>(N, K, ntiles, hist, offs);
+  k_csort_scatter<<<dim3((ntiles + 3) / 4, BH), 128, 4 * K * sizeof(int), st>>>(lab, N, K, ntiles,
+                                                                               hist, perm);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_permute_rows(XView x, int BH, int N, int d, const int32_t* perm,
+                                __nv_bfloat16* xp, cudaStream_t st) {
+  const int rows_per_block = 256 / (d / 8);
+  k_permute_rows<<<dim3((N + rows_per_block - 1) / rows_per_block, BH), 256, 0, st>>>(x, N, d, perm, xp);
+  return cudaGetLastError();
+}
+
+}  // namespace cs

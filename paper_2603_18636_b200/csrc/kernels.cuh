@@ -1,0 +1,64 @@
+// kernels.cuh — declarations shared by the libcoclust translation units.
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <type_traits>
+
+#include "common.cuh"
+
+namespace cs {
+
+constexpr int kSortTile = 1024;  // tokens per counting-sort tile
+constexpr int kMaxClusters = 1024;
+
+// Strided bf16 [B, H, N, d] view (d contiguous).
+struct XView {
+  const __nv_bfloat16* p;
+  long long sb, sh, sn;
+  int H;
+  __device__ __forceinline__ const __nv_bfloat16* row(int b, int h, int n) const {
+    return p + (long long)b * sb + (long long)h * sh + (long long)n * sn;
+  }
+};
+
+// ---- cluster.cu
+cudaError_t launch_init_sample(XView q, XView k, int BH, int N, int d, int kq, int kk,
+                               unsigned long long seed, int h_off, int h_tot, const int32_t* init_q,
+                               const int32_t* init_k, float* cq, float* ck, cudaStream_t st);
+cudaError_t launch_anchor_prep(const float* ca, int ka, const float* cself, int ks, int ks_pad,
+                               int BH, int d, double* gamma, __nv_bfloat16* wsplit, cudaStream_t st);
+cudaError_t launch_seg_mean(XView x, int BH, int N, int d, int K, const int32_t* perm,
+                            const int32_t* offs, float* C, __nv_bfloat16* xperm, cudaStream_t st);
+cudaError_t launch_csort(const int32_t* lab, int BH, int N, int K, int32_t* perm, int32_t* offs,
+                         int32_t* hist, cudaStream_t st);
+cudaError_t launch_permute_rows(XView x, int BH, int N, int d, const int32_t* perm,
+                                __nv_bfloat16* xp, cudaStream_t st);
+
+// ---- assign.cu : labels[bh][n] = argmax_j x_n . W_j  (tcgen05 GEMM + fused argmax epilogue)
+// tm_x: 4D map over x {d, N, H, B} box {64, 128, 1, 1}; tm_w: 2D map over Wsplit {2d, BH*ks_pad}
+// box {64, nch}.
+cudaError_t launch_assign_gemm(const CUtensorMap* tm_x, const CUtensorMap* tm_w, int B, int H, int N,
+                               int d, int ks, int nch, int ks_pad, int32_t* labels, cudaStream_t st);
+
+// ---- select.cu
+cudaError_t launch_block_select(int BH, int H, int kq, int kk, int d, const float* cq,
+                                const float* ck, const int32_t* offs_q, const int32_t* offs_k,
+                                const float* budget, double tau, double theta, int rule,
+                                int32_t* n_keep, int32_t* kept, int32_t* order, int32_t* cnt,
+                                cudaStream_t st);
+cudaError_t launch_worklist(int BH, int kq, const int32_t* offs_q, int32_t* item_start,
+                            cudaStream_t st);
+int worklist_upper_bound(int N, int kq);
+
+// ---- attn.cu : block-sparse flash attention over cluster-sorted Q/K/V (bf16 [BH, N, d])
+cudaError_t launch_bsa_fwd(const CUtensorMap* tm_q, const CUtensorMap* tm_k, const CUtensorMap* tm_v,
+                           int BH, int H, int N, int d, int kq, int kk, const int32_t* perm_q,
+                           const int32_t* offs_q, const int32_t* offs_k, const int32_t* n_keep,
+                           const int32_t* kept, const int32_t* item_start, int items_ub,
+                           float scale, __nv_bfloat16* o, long long osb, long long osh,
+                           long long osn, cudaStream_t st);
+
+}  // namespace cs

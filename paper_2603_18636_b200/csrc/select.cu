@@ -1,0 +1,251 @@
+// select.cu — top block-pair selection and the attention work list.
+//   k_select_rows : per (bh, query block a): Abar_a = C_q[a] C_k^T (fp64, empty key blocks -> -inf),
+//                   order = key blocks by (Abar desc, index asc) (bitonic sort in SMEM),
+//                   c_a = min{m : cumsum of softmax(Abar_a / sqrt(d)) over that order >= tau-1e-12}
+//   k_select_count: per bh: n_rec = ceil(sum c_a / Kq'), rule (R8, R10) -> n_keep
+//   k_select_emit : kept[a] = the first n_keep of order[a], ascending
+//   k_worklist    : per bh, exclusive scan of ceil(ceil(|Q_a|/128)/2) -> attention work items
+#include <float.h>
+
+#include "kernels.cuh"
+
+namespace cs {
+
+__device__ __forceinline__ bool before(double va, int ia, double vb, int ib) {
+  return va > vb || (va == vb && ia < ib);
+}
+
+// grid (kq, BH), block 256, dyn smem: P2 doubles + P2 ints + d doubles
+__global__ void __launch_bounds__(256) k_select_rows(int kq, int kk, int d, const float* __restrict__ cq,
+                                                     const float* __restrict__ ck,
+                                                     const int32_t* __restrict__ offs_q,
+                                                     const int32_t* __restrict__ offs_k, double tau,
+                                                     int32_t* __restrict__ order, int32_t* __restrict__ cnt) {
+  extern __shared__ double sh_d[];
+  __shared__ double wred[8];
+  __shared__ int first_hit;
+  int P2 = 1;
+  while (P2 < kk) P2 <<= 1;
+  double* sval = sh_d;
+  double* scq = sh_d + P2;
+  int* sidx = reinterpret_cast<int*>(scq + d);
+  const int a = blockIdx.x, bh = blockIdx.y, t = threadIdx.x;
+  const int32_t* ok = offs_k + (size_t)bh * (kk + 1);
+  const int32_t* oq = offs_q + (size_t)bh * (kq + 1);
+  const float* crow = cq + ((size_t)bh * kq + a) * d;
+  for (int e = t; e < d; e += 256) scq[e] = (double)crow[e];
+  __syncthreads();
+  for (int j = t; j < P2; j += 256) {
+    double v = -INFINITY;
+    if (j < kk && ok[j + 1] - ok[j] > 0) {
+      const float* kr = ck + ((size_t)bh * kk + j) * d;
+      double acc = 0.0;
+      for (int e = 0; e < d; ++e) acc = fma(scq[e], (double)kr[e], acc);
+      v = acc;
+    }
+    sval[j] = v;
+    sidx[j] = j;
+  }
+  __syncthreads();
+  // bitonic sort: (value desc, index asc)
+  for (int size = 2; size <= P2; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = t; i < P2; i += 256) {
+        const int jx = i ^ stride;
+        if (jx > i) {
+          const bool up = (i & size) == 0;  // "up" segments sorted by `before`
+          const double vi = sval[i], vj = sval[jx];
+          const int ii = sidx[i], ij = sidx[jx];
+          const bool swap = up ? before(vj, ij, vi, ii) : before(vi, ii, vj, ij);
+          if (swap) { sval[i] = vj; sval[jx] = vi; sidx[i] = ij; sidx[jx] = ii; }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // number of nonempty key blocks
+  int ne = 0;
+  for (int j = t; j < kk; j += 256) ne += (ok[j + 1] - ok[j] > 0) ? 1 : 0;
+  ne = warp_sum(ne);
+  __shared__ int sne[8];
+  if ((t & 31) == 0) sne[t >> 5] = ne;
+  __syncthreads();
+  int kne = 0;
+  for (int w = 0; w < 8; ++w) kne += sne[w];
+  int32_t* ord = order + ((size_t)bh * kq + a) * kk;
+  for (int j = t; j < kk; j += 256) ord[j] = sidx[j];
+  const bool q_nonempty = oq[a + 1] - oq[a] > 0;
+  if (!q_nonempty || kne == 0) {
+    if (t == 0) cnt[(size_t)bh * kq + a] = 0;
+    return;
+  }
+  // softmax over the kne nonempty entries (sorted prefix), then the cumulative mass
+  const double sd = sqrt((double)d);
+  const double mz = sval[0] / sd;
+  // each thread owns 4 consecutive sorted entries (P2 <= 1024)
+  const int per = (P2 + 255) / 256;
+  double e_loc[4];
+  double s_loc = 0.0;
+  for (int u = 0; u < per; ++u) {
+    const int i = t * per + u;
+    e_loc[u] = (i < kne) ? exp(sval[i] / sd - mz) : 0.0;
+    s_loc += e_loc[u];
+  }
+  // block sum (fixed tree order)
+  double tot = s_loc;
+  for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+  if ((t & 31) == 0) wred[t >> 5] = tot;
+  __syncthreads();
+  double total = 0.0;
+  for (int w = 0; w < 8; ++w) total += wred[w];
+  __syncthreads();
+  // exclusive scan of the per-thread sums of p
+  double p_loc = 0.0;
+  for (int u = 0; u < per; ++u) { e_loc[u] /= total; p_loc += e_loc[u]; }
+  double x = p_loc;
+  for (int o = 1; o < 32; o <<= 1) {
+    const double y = __shfl_up_sync(0xffffffffu, x, o);
+    if ((t & 31) >= o) x += y;
+  }
+  if ((t & 31) == 31) wred[t >> 5] = x;
+  if (t == 0) first_hit = kne;
+  __syncthreads();
+  double base = 0.0;
+  for (int w = 0; w < (t >> 5); ++w) base += wred[w];
+  double cs_ = base + x - p_loc;
+  const double thr = tau - 1e-12;
+  for (int u = 0; u < per; ++u) {
+    const int i = t * per + u;
+    cs_ += e_loc[u];
+    if (i < kne && cs_ >= thr) { atomicMin(&first_hit, i + 1); break; }
+  }
+  __syncthreads();
+  if (t == 0) cnt[(size_t)bh * kq + a] = first_hit;
+}
+
+__device__ __forceinline__ int n_from_ratio(double r, int kk) {
+  int n = (int)ceil(r * (double)kk - 1e-3);
+  return min(max(n, 1), kk);
+}
+
+// grid BH, block 1024
+__global__ void __launch_bounds__(1024) k_select_count(int H, int kq, int kk,
+                                                       const int32_t* __restrict__ offs_q,
+                                                       const int32_t* __restrict__ offs_k,
+                                                       const int32_t* __restrict__ cnt,
+                                                       const float* __restrict__ budget, double theta,
+                                                       int rule, int32_t* __restrict__ n_keep) {
+  __shared__ int s_sum[32], s_nq[32], s_nk[32];
+  const int bh = blockIdx.x, t = threadIdx.x;
+  const int32_t* oq = offs_q + (size_t)bh * (kq + 1);
+  const int32_t* ok = offs_k + (size_t)bh * (kk + 1);
+  int sum = 0, nq = 0, nk = 0;
+  for (int a = t; a < kq; a += 1024) {
+    if (oq[a + 1] - oq[a] > 0) { ++nq; sum += cnt[(size_t)bh * kq + a]; }
+  }
+  for (int j = t; j < kk; j += 1024) nk += (ok[j + 1] - ok[j] > 0) ? 1 : 0;
+  sum = warp_sum(sum); nq = warp_sum(nq); nk = warp_sum(nk);
+  if ((t & 31) == 0) { s_sum[t >> 5] = sum; s_nq[t >> 5] = nq; s_nk[t >> 5] = nk; }
+  __syncthreads();
+  if (t == 0) {
+    int S = 0, NQ = 0, NK = 0;
+    for (int w = 0; w < 32; ++w) { S += s_sum[w]; NQ += s_nq[w]; NK += s_nk[w]; }
+    const int n_rec = NQ > 0 ? (S + NQ - 1) / NQ : 1;
+    const double b = (double)budget[bh % H];
+    const int n_b = n_from_ratio(b, kk);
+    int n;
+    if (rule == 0) n = (1.0 - b) > theta ? min(n_rec, n_b) : max(n_rec, n_b);
+    else if (rule == 1) n = b > theta ? min(n_rec, n_b) : max(n_rec, n_b);
+    else n = n_b;
+    n = min(max(n, 1), max(NK, 1));
+    n_keep[bh] = n;
+  }
+}
+
+// grid (kq, BH), block 256: kept row = first n of order, ascending
+__global__ void __launch_bounds__(256) k_select_emit(int kq, int kk, const int32_t* __restrict__ order,
+                                                     const int32_t* __restrict__ n_keep,
+                                                     int32_t* __restrict__ kept) {
+  __shared__ uint32_t flags[kMaxClusters / 32];
+  __shared__ int sbuf[32];
+  const int a = blockIdx.x, bh = blockIdx.y, t = threadIdx.x;
+  const int n = n_keep[bh];
+  for (int w = t; w < kMaxClusters / 32; w += 256) flags[w] = 0u;
+  __syncthreads();
+  const int32_t* ord = order + ((size_t)bh * kq + a) * kk;
+  for (int i = t; i < n; i += 256) {
+    const int j = ord[i];
+    atomicOr(&flags[j >> 5], 1u << (j & 31));
+  }
+  __syncthreads();
+  // each thread owns 4 consecutive indices
+  int c = 0;
+  for (int u = 0; u < 4; ++u) {
+    const int j = t * 4 + u;
+    c += (j < kk && ((flags[j >> 5] >> (j & 31)) & 1u)) ? 1 : 0;
+  }
+  // block exclusive scan (256 threads)
+  const int lane = t & 31, w = t >> 5;
+  int x = c;
+  for (int o = 1; o < 32; o <<= 1) { int y = __shfl_up_sync(0xffffffffu, x, o); if (lane >= o) x += y; }
+  if (lane == 31) sbuf[w] = x;
+  __syncthreads();
+  int base = 0;
+  for (int ww = 0; ww < w; ++ww) base += sbuf[ww];
+  int pos = base + x - c;
+  int32_t* out = kept + ((size_t)bh * kq + a) * kk;
+  for (int u = 0; u < 4; ++u) {
+    const int j = t * 4 + u;
+    if (j < kk && ((flags[j >> 5] >> (j & 31)) & 1u)) out[pos++] = j;
+  }
+}
+
+// grid BH, block 1024 (kq <= 1024): item_start[bh][a] (pairs of 128-row query tiles)
+__global__ void __launch_bounds__(1024) k_worklist(int kq, const int32_t* __restrict__ offs_q,
+                                                   int32_t* __restrict__ item_start) {
+  extern __shared__ int sbuf_w[];
+  const int bh = blockIdx.x, a = threadIdx.x;
+  const int32_t* oq = offs_q + (size_t)bh * (kq + 1);
+  int items = 0;
+  if (a < kq) {
+    const int len = oq[a + 1] - oq[a];
+    const int tiles = (len + 127) / 128;
+    items = (tiles + 1) / 2;
+  }
+  // block exclusive scan
+  const int lane = a & 31, w = a >> 5;
+  int x = items;
+  for (int o = 1; o < 32; o <<= 1) { int y = __shfl_up_sync(0xffffffffu, x, o); if (lane >= o) x += y; }
+  if (lane == 31) sbuf_w[w] = x;
+  __syncthreads();
+  int base = 0;
+  for (int ww = 0; ww < w; ++ww) base += sbuf_w[ww];
+  int32_t* is = item_start + (size_t)bh * (kq + 1);
+  if (a < kq) is[a] = base + x - items;
+  if (a == kq - 1) is[kq] = base + x;
+}
+
+int worklist_upper_bound(int N, int kq) { return (N + 255) / 256 + kq; }
+
+cudaError_t launch_block_select(int BH, int H, int kq, int kk, int d, const float* cq,
+                                const float* ck, const int32_t* offs_q, const int32_t* offs_k,
+                                const float* budget, double tau, double theta, int rule,
+                                int32_t* n_keep, int32_t* kept, int32_t* order, int32_t* cnt,
+                                cudaStream_t st) {
+  int P2 = 1;
+  while (P2 < kk) P2 <<= 1;
+  const size_t smem = (size_t)P2 * 8 + (size_t)d * 8 + (size_t)P2 * 4;
+  k_select_rows<<<dim3(kq, BH), 256, smem, st>>>(kq, kk, d, cq, ck, offs_q, offs_k, tau, order, cnt);
+  k_select_count<<<BH, 1024, 0, st>>>(H, kq, kk, offs_q, offs_k, cnt, budget, theta, rule, n_keep);
+  k_select_emit<<<dim3(kq, BH), 256, 0, st>>>(kq, kk, order, n_keep, kept);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_worklist(int BH, int kq, const int32_t* offs_q, int32_t* item_start,
+                            cudaStream_t st) {
+  const int threads = ((kq + 31) / 32) * 32;
+  k_worklist<<<BH, threads, 32 * sizeof(int), st>>>(kq, offs_q, item_start);
+  return cudaGetLastError();
+}
+
+}  // namespace cs
