@@ -1,0 +1,358 @@
+#!/usr/bin/env python
+"""bench.py — SVOO co-clustered block-sparse attention layer on B200 (BASELINE.json configs[2]).
+
+One step = one pass of the whole hot path over one attention layer (all of this rank's heads):
+online co-clustering (I_max iterations) -> permutation -> block selection -> block-sparse
+attention with the inverse permutation fused.  Metric = ms per attention layer (lower is better),
+plus dense-equivalent TFLOP/s.  Multi-GPU: head-parallel (rank r owns heads [rH/P, (r+1)H/P)),
+no collective on the data path; time = max over ranks.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config ...]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ms per attention layer + dense-equiv TFLOP/s, Wan2.1-14B 720p, 1/2/4/8 B200"
+CONFIG_NAMES = {"wan14b_720p": "Wan2.1-14B 720p attention (BASELINE configs[2])",
+                "wan1.3b_480p": "Wan2.1-1.3B 480p attention (BASELINE configs[1])",
+                "hunyuan_720p": "HunyuanVideo 720p attention (BASELINE configs[3])",
+                "toy": "toy (BASELINE configs[0])"}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="wan14b_720p")
+    ap.add_argument("--kq", type=int, default=100)
+    ap.add_argument("--kk", type=int, default=500)
+    ap.add_argument("--iters", type=int, default=2)
+    ap.add_argument("--budget", type=float, default=0.2)
+    ap.add_argument("--rule", choices=["fixed", "density", "as_written"], default="fixed")
+    ap.add_argument("--tau", type=float, default=0.95)
+    ap.add_argument("--theta", type=float, default=0.1)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-sample-rows", type=int, default=1500,
+                    help="query rows of the oracle attention sample")
+    return ap.parse_args()
+
+
+RULES = {"density": 0, "as_written": 1, "fixed": 2}
+
+
+def dist_init(args):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl" if args.impl == "ours" else "gloo")
+    return ws, rank, local
+
+
+def head_range(H, world, rank):
+    base, rem = divmod(H, world)
+    lo = rank * base + min(rank, rem)
+    return lo, lo + base + (1 if rank < rem else 0)
+
+
+# ------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = f"/tmp/bench_clocks_{os.getpid()}.csv"
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                rows.append(parts)
+        if not rows:
+            return None
+        sm = sorted(float(r[1]) for r in rows if r[1].replace(".", "").isdigit())
+        mx = max(float(r[2]) for r in rows if r[2].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ------------------------------------------------------------------------------ oracle baseline
+def cpu_oracle_sample(w, h, kq, kk, iters, budget, rule, tau, theta, seed, H_total, rows):
+    """Time the float64 oracle on one head: full co-clustering + selection, attention on a row
+    sample; returns (extrapolated ms per layer, details)."""
+    import numpy as np
+    from oracle import svoo
+    f = lambda t: t.float().cpu().double().numpy()
+    Q, K, V = f(w.q[0, h]), f(w.k[0, h]), f(w.v[0, h])
+    N, d = Q.shape
+    t0 = time.perf_counter()
+    cc = svoo.cocluster(Q, K, kq, kk, iters, seed=seed, h=h, H=H_total)
+    pq, oq = svoo.counting_sort(cc.Lq, kq)
+    pk, ok = svoo.counting_sort(cc.Lk, kk)
+    sel = svoo.select_blocks(cc.Cq, cc.Ck, np.diff(oq), np.diff(ok), budget, tau, theta, rule, d_head=d)
+    t1 = time.perf_counter()
+    rs = np.random.default_rng(0).choice(N, size=min(rows, N), replace=False)
+    Lq, Lk = cc.Lq, cc.Lk
+    t2 = time.perf_counter()
+    for a in np.unique(Lq[rs]):
+        rr = rs[Lq[rs] == a]
+        svoo.sparse_attention(Q[rr], K, V, np.zeros(len(rr), np.int64), Lk, {0: sel.kept[a]})
+    t3 = time.perf_counter()
+    per_head_s = (t1 - t0) + (t3 - t2) * N / len(rs)
+    return per_head_s * H_total * 1e3, dict(cluster_s=t1 - t0, attn_sample_s=t3 - t2, rows=len(rs))
+
+
+def run_reference(args):
+    """--impl reference: the float64 oracle as it stands, on this host's cores."""
+    import torch
+    from synthetic import CONFIGS, video_qkv
+    world, rank, local = dist_init(args)
+    if rank != 0:
+        return
+    c = CONFIGS[args.config]
+    H = c["H"]
+    w = video_qkv(c["T"], c["Hs"], c["Ws"], 1, c["d"], seed=args.seed, layer=0)  # head 0 stream
+    cores = len(os.sched_getaffinity(0))
+    rows = max(64, args.cpu_sample_rows // 3)
+    for _ in range(args.warmup):
+        cpu_oracle_sample(w, 0, args.kq, args.kk, 1, args.budget, RULES[args.rule], args.tau, args.theta,
+                          args.seed, H, 64)
+    vals = []
+    for _ in range(args.steps):
+        v, det = cpu_oracle_sample(w, 0, args.kq, args.kk, args.iters, args.budget, RULES[args.rule],
+                                   args.tau, args.theta, args.seed, H, rows)
+        vals.append(v)
+    ms = sum(vals) / len(vals)
+    N, d = w.q.shape[2], w.q.shape[3]
+    sample = (f"1 of {H} heads: full co-clustering ({args.iters} it, {args.kq}/{args.kk}) + selection, "
+              f"attention on {rows} random query rows; extrapolated x N/rows x H")
+    line = {"impl": "reference", "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "dense_equiv_tflops": 4.0 * H * N * N * d / (ms * 1e-3) / 1e12,
+            "config": {"workload": CONFIG_NAMES[args.config], "H": H, "N": N, "d": d, "kq": args.kq,
+                       "kk": args.kk, "iters": args.iters, "budget": args.budget, "rule": args.rule},
+            "cpu_baseline": {"value": ms, "unit": "ms", "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": ms, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------ ours
+def run_ours(args):
+    import numpy as np
+    import torch
+    import paper_2603_18636_b200 as pb
+    from synthetic import CONFIGS, video_qkv
+
+    world, rank, local = dist_init(args)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    c = CONFIGS[args.config]
+    H_total, d = c["H"], c["d"]
+    h0, h1 = head_range(H_total, world, rank)
+    # deterministic per-head generation: every rank builds exactly its heads of the full layer
+    full = video_qkv(c["T"], c["Hs"], c["Ws"], H_total, d, seed=args.seed, device=dev) if world == 1 else None
+    if full is None:
+        parts = [video_qkv(c["T"], c["Hs"], c["Ws"], H_total, d, seed=args.seed, device=dev)]
+        q, k, v = (t[:, h0:h1].contiguous() for t in (parts[0].q, parts[0].k, parts[0].v))
+        del parts
+    else:
+        q, k, v = full.q, full.k, full.v
+    B, H, N, _ = q.shape
+    budget = torch.full((H,), args.budget, dtype=torch.float32, device=dev)
+    rule = RULES[args.rule]
+    ws = pb.Workspace()
+    out = torch.empty_like(q)
+    kw = dict(seed=args.seed, tau=args.tau, theta=args.theta, rule=rule, out=out, ws=ws, head_offset=h0,
+              heads_total=H_total)
+
+    def step(evs=None):
+        pb.coclust_sparse_attention(q, k, v, args.kq, args.kk, args.iters, budget, stage_events=evs, **kw)
+
+    # kept FLOPs of this layer (state recomputed through the staged entries: same kernels, same bits)
+    st = pb.coclust_assign(q, k, args.kq, args.kk, args.iters, seed=args.seed, ws=ws, head_offset=h0,
+                           heads_total=H_total)
+    n_keep, kept = pb.block_select(st["cq"], st["ck"], st["offs_q"], st["offs_k"], budget, args.tau,
+                                   args.theta, rule, ws=ws)
+    torch.cuda.synchronize()
+    oq = st["offs_q"].cpu().numpy().reshape(B * H, -1)
+    ok = st["offs_k"].cpu().numpy().reshape(B * H, -1)
+    kp = kept.cpu().numpy().reshape(B * H, args.kq, args.kk)
+    nk = n_keep.cpu().numpy().reshape(-1)
+    f_kept = 0
+    for bh in range(B * H):
+        sq, sk = np.diff(oq[bh]), np.diff(ok[bh])
+        f_kept += int((sq * sk[kp[bh, :, :nk[bh]]].sum(1)).sum())
+    f_kept *= 4 * d
+    del st, n_keep, kept
+
+    for _ in range(max(args.warmup, 1)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    K = args.steps
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    torch.cuda.synchronize()
+    t_start.record()
+    step_starts = []
+    for i in range(K):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        step_starts.append(e0)
+        step(evs[i])
+    t_end.record()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms = t_start.elapsed_time(t_end) / K
+    st_cluster = sum(step_starts[i].elapsed_time(evs[i][0]) for i in range(K)) / K
+    st_select = sum(evs[i][0].elapsed_time(evs[i][1]) for i in range(K)) / K
+    st_prep = sum(evs[i][1].elapsed_time(evs[i][2]) for i in range(K)) / K
+    t_attn = sum(evs[i][2].elapsed_time(evs[i][3]) for i in range(K)) / K
+    if world > 1:
+        tt = torch.tensor([ms, t_attn], device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        ms, t_attn_max = float(tt[0]), float(tt[1])
+        fk = torch.tensor([float(f_kept)], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(fk)
+        f_kept_total = float(fk[0])
+    else:
+        f_kept_total = float(f_kept)
+
+    # ---- e2e: host buffers in, host buffer out, through the same public call
+    e2e = None
+    if not args.no_e2e:
+        hq, hk, hv = (t.cpu().pin_memory() for t in (q, k, v))
+        ho = torch.empty(out.shape, dtype=out.dtype).pin_memory()
+        dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+        def e2e_step():
+            dq.copy_(hq, non_blocking=True); dk.copy_(hk, non_blocking=True); dv.copy_(hv, non_blocking=True)
+            pb.coclust_sparse_attention(dq, dk, dv, args.kq, args.kk, args.iters, budget, **kw)
+            ho.copy_(out, non_blocking=True)
+        e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(K):
+            e2e_step()
+        b_.record()
+        torch.cuda.synchronize()
+        e2e_ms = a.elapsed_time(b_) / K
+        if world > 1:
+            tt = torch.tensor([e2e_ms], device=dev)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            e2e_ms = float(tt[0])
+        nbytes = q.numel() * 2
+        e2e = {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": 3 * nbytes * world,
+               "d2h_bytes_per_step": nbytes * world}
+        del hq, hk, hv, ho, dq, dk, dv
+
+    if rank != 0:
+        return
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    peak_sust = peaks.get("bf16_tflops_sustained", 1400.0)
+    peak_burst = peaks.get("bf16_tflops", 1590.0)
+    f_local = float(f_kept)
+    achieved = f_local / (t_attn * 1e-3) / 1e12
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "attn_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            tj = json.load(open(tpath))
+            if tj.get("config") == args.config and abs(tj.get("budget", -1) - args.budget) < 1e-9:
+                traffic = tj.get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    dense_flops = 4.0 * B * H_total * N * N * d
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        v_ms, det = cpu_oracle_sample(full, 0, args.kq, args.kk, args.iters, args.budget, rule, args.tau,
+                                      args.theta, args.seed, H_total, args.cpu_sample_rows)
+        cpu = {"value": v_ms, "unit": "ms", "cores": len(os.sched_getaffinity(0)), "kind": "oracle",
+               "sample": (f"head 0 of {H_total}: full float64 co-clustering ({args.iters} it, {args.kq}/"
+                          f"{args.kk}) + selection ({det['cluster_s']:.1f} s) and attention on "
+                          f"{det['rows']} random query rows ({det['attn_sample_s']:.1f} s); "
+                          f"extrapolated x N/rows, x H (ms per layer)")}
+    line = {
+        "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world, "steps": K, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+        "dtype": "bf16", "data": "synthetic",
+        "dense_equiv_tflops": dense_flops / (ms * 1e-3) / 1e12,
+        "config": {"workload": CONFIG_NAMES[args.config], "B": B, "H": H_total, "N": N, "d": d,
+                   "kq": args.kq, "kk": args.kk, "iters": args.iters, "budget": args.budget,
+                   "rule": args.rule, "tau": args.tau, "theta": args.theta,
+                   "parallelism": f"head-parallel x{world}", "l2": "inputs larger than L2 (%.0f MB/tensor)"
+                   % (q.numel() * 2 / 1e6)},
+        "kept_tflop_per_layer": f_kept_total / 1e12,
+        "kept_frac": f_kept_total / dense_flops,
+        "stages_ms": {"cocluster": st_cluster, "select": st_select, "permute_v_worklist": st_prep,
+                      "attention": t_attn},
+        "roofline": {"kernel": "k_bsa_fwd", "bound": "tensor", "achieved": achieved, "peak": peak_sust,
+                     "unit": "TFLOP/s", "frac": achieved / peak_sust, "frac_of_burst": achieved / peak_burst,
+                     "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside a long step)",
+                     "traffic": traffic,
+                     "algorithmic": "kept FLOPs 4*d*sum_a |Q_a| sum_{c in kept[a]} |K_c| per launch (rank 0)"},
+        "layer_kept_tflops": f_kept_total / (ms * 1e-3) / 1e12,
+        "gpu_launches": pb.launches_per_layer(args.iters) * K,
+        "clocks": clk, "e2e": e2e, "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        import torch.distributed as dist
+        if dist.is_initialized():
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

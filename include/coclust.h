@@ -138,13 +138,15 @@ cs_status block_sparse_attn(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in
 
 /* The whole layer: coclust_assign -> block_select -> block_sparse_attn, on device only (no host
  * round trip; CUDA-graph capturable).  budget [H] is indexed by the local head h; head_offset /
- * heads_total as in coclust_assign. */
+ * heads_total as in coclust_assign.  stage_events (nullable) = 4 cudaEvent_t recorded on `stream`
+ * (0) after co-clustering, (1) after block selection, (2) just before and (3) just after the
+ * block-sparse attention kernel — for per-stage timing by the caller. */
 cs_status coclust_sparse_attention(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in k,
                                    cs_bf16_in v, int kq, int kk, int iters, uint64_t seed,
                                    int head_offset, int heads_total,
                                    const float* budget, double tau, double theta, int rule,
                                    float scale, cs_bf16_out o, void* ws, size_t ws_bytes,
-                                   void* stream);
+                                   void* stream, void* const* stage_events);
 
 #ifdef __cplusplus
 }

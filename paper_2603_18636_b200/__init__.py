@@ -58,7 +58,7 @@ _SIG = {
                                _P, ctypes.c_float, _BF16Out, _P, ctypes.c_size_t, _P]),
     "coclust_sparse_attention": (_I, [_I, _I, _I, _I, _BF16In, _BF16In, _BF16In, _I, _I, _I,
                                       ctypes.c_uint64, _I, _I, _P, ctypes.c_double, ctypes.c_double, _I,
-                                      ctypes.c_float, _BF16Out, _P, ctypes.c_size_t, _P]),
+                                      ctypes.c_float, _BF16Out, _P, ctypes.c_size_t, _P, _P]),
 }
 
 _lib = None
@@ -103,6 +103,13 @@ def _bf16(t: torch.Tensor, out: bool = False):
 def _cuda(t: torch.Tensor, name: str):
     if not t.is_cuda:
         raise ValueError(f"{name} must be a CUDA tensor (no CPU fallback)")
+
+
+def launches_per_layer(iters: int) -> int:
+    """Kernels the fused entry launches per layer: init_sample 1; per iteration and side: anchor
+    prep 2 + assign GEMM 1 + counting sort 3 + centroid update 1; selection 3; V permute 1;
+    work list 1; attention 1."""
+    return 1 + iters * 2 * 7 + 3 + 1 + 1 + 1
 
 
 def workspace_bytes(B, H, N, d, kq, kk) -> int:
@@ -214,14 +221,19 @@ def block_sparse_attn(q, k, v, perm_q, offs_q, perm_k, offs_k, n_keep, kept, sca
 
 def coclust_sparse_attention(q, k, v, kq, kk, iters, budget, *, seed=0, tau=0.95, theta=0.1,
                              rule=RULE_DENSITY, scale=None, out=None, ws=None, head_offset=0,
-                             heads_total=0):
+                             heads_total=0, stage_events=None):
+    """stage_events: optional 4 torch.cuda.Event (enable_timing) recorded after co-clustering,
+    after selection, and around the attention kernel."""
     """The whole SVOO attention layer (north_star stages 1-5) on device."""
     _cuda(q, "q")
     B, H, N, d = q.shape
     scale = d ** -0.5 if scale is None else scale
     out = torch.empty(B, H, N, d, dtype=torch.bfloat16, device=q.device) if out is None else out
     w, wn = _ws(ws, workspace_bytes(B, H, N, d, kq, kk), q.device)
+    evs = None
+    if stage_events is not None:
+        evs = (ctypes.c_void_p * 4)(*[ctypes.c_void_p(e.cuda_event) for e in stage_events])
     _check(lib().coclust_sparse_attention(B, H, N, d, _bf16(q), _bf16(k), _bf16(v), kq, kk, iters,
                                           seed, head_offset, heads_total, _ptr(budget), float(tau), float(theta), int(rule),
-                                          float(scale), _bf16(out, True), w, wn, _stream(q)))
+                                          float(scale), _bf16(out, True), w, wn, _stream(q), evs))
     return out

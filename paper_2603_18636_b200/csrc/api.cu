@@ -252,17 +252,19 @@ cs_status run_assign(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in k, int
 
 cs_status run_attn(int B, int H, int N, int d, int kq, int kk, const int32_t* perm_q, const int32_t* offs_q,
                    const int32_t* offs_k, const int32_t* n_keep, const int32_t* kept, float scale,
-                   cs_bf16_out o, const AttnScratch& sc, cudaStream_t st) {
+                   cs_bf16_out o, const AttnScratch& sc, cudaStream_t st, void* const* ev = nullptr) {
   const int BH = B * H;
   CS_CUDA(launch_worklist(BH, kq, offs_q, sc.item_start, st), "worklist");
   CUtensorMap tq, tk, tv;
   CS_CHECK(make_map_2d(&tq, sc.qp, (uint64_t)BH * N, d, 128));
   CS_CHECK(make_map_2d(&tk, sc.kp, (uint64_t)BH * N, d, 8));
   CS_CHECK(make_map_2d(&tv, sc.vp, (uint64_t)BH * N, d, 8));
+  if (ev) CS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(ev[2]), st), "event");
   CS_CUDA(launch_bsa_fwd(&tq, &tk, &tv, BH, H, N, d, kq, kk, perm_q, offs_q, offs_k, n_keep, kept,
                          sc.item_start, worklist_upper_bound(N, kq), scale,
                          static_cast<__nv_bfloat16*>(o.ptr), o.sb, o.sh, o.sn, st),
           "bsa_fwd");
+  if (ev) CS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(ev[3]), st), "event");
   return CS_OK;
 }
 
@@ -423,7 +425,8 @@ cs_status block_sparse_attn(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in
 cs_status coclust_sparse_attention(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in k, cs_bf16_in v, int kq,
                                    int kk, int iters, uint64_t seed, int head_offset, int heads_total,
                                    const float* budget, double tau, double theta,
-                                   int rule, float scale, cs_bf16_out o, void* ws, size_t ws_bytes, void* stream) {
+                                   int rule, float scale, cs_bf16_out o, void* ws, size_t ws_bytes, void* stream,
+                                   void* const* stage_events) {
   g_err[0] = 0;
   CS_CHECK(check_dims(B, H, N, d));
   CS_CHECK(check_k(kq, N, "kq"));
@@ -449,11 +452,14 @@ cs_status coclust_sparse_attention(int B, int H, int N, int d, cs_bf16_in q, cs_
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   CS_CHECK(run_assign(B, H, N, d, q, k, kq, kk, iters, seed, head_offset, heads_total, nullptr, nullptr, s.cq, s.ck, s.lq, s.lk, s.perm_q,
                       s.offs_q, s.perm_k, s.offs_k, as, at.qp, at.kp, st));
+  if (stage_events) CS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(stage_events[0]), st), "event");
   CS_CUDA(launch_block_select(BH, H, kq, kk, d, s.cq, s.ck, s.offs_q, s.offs_k, budget, tau, theta, rule,
                               s.n_keep, s.kept, se.order, se.cnt, st),
           "block_select");
+  if (stage_events) CS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(stage_events[1]), st), "event");
   CS_CUDA(launch_permute_rows(view(v, H), BH, N, d, s.perm_k, at.vp, st), "permute_v");
-  return run_attn(B, H, N, d, kq, kk, s.perm_q, s.offs_q, s.offs_k, s.n_keep, s.kept, scale, o, at, st);
+  return run_attn(B, H, N, d, kq, kk, s.perm_q, s.offs_q, s.offs_k, s.n_keep, s.kept, scale, o, at, st,
+                  stage_events);
 }
 
 }  // extern "C"

@@ -265,6 +265,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           l *= alpha;
           m = mx;
         }
+        // tcgen05.ld/st are warp-collective (.sync.aligned): rescale if any row of the warp needs it
+        const bool warp_rescale = __any_sync(0xffffffffu, alpha != 1.f);
         float rs = 0.f;
 #pragma unroll
         for (int c = 0; c < BN; c += 2) {
@@ -275,7 +277,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         l += rs;
         tmem_st32(s_tm, su);
         tmem_st32(s_tm + 32, su + 32);
-        if (alpha != 1.f) {  // lazy O rescale; PV(j) is not issued before p_full(j)
+        if (warp_rescale) {  // lazy O rescale; PV(j) is not issued before p_full(j)
 #pragma unroll 1
           for (int c = 0; c < D / 32; ++c) {
             uint32_t ov[32];

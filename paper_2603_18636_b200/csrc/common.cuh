@@ -47,8 +47,13 @@ CS_DEV bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// Spin until the phase with `parity` completes.  A wait that exceeds ~2^35 cycles (~20 s) can
+// only be a deadlock: trap so the launch fails loudly instead of hanging the GPU.
 CS_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+  if (mbar_try_wait(bar, parity)) return;
+  const long long t0 = clock64();
   while (!mbar_try_wait(bar, parity)) {
+    if (clock64() - t0 > (1LL << 35)) __trap();
   }
 }
 

@@ -99,7 +99,7 @@ def test_attention_argument_errors(L):
                              0.0, o, FAKE, 1 << 40, None)
     assert st == 3  # scale must be > 0
     st = L.coclust_sparse_attention(1, 1, 256, 128, q, q, q, 16, 16, 2, 0, 0, 0, None, 0.95, 0.1, 0,
-                                    0.1, o, FAKE, 1 << 40, None)
+                                    0.1, o, FAKE, 1 << 40, None, None)
     assert st == 1  # budget NULL
 
 
