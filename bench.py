@@ -229,6 +229,9 @@ def run_ours(args):
         torch.distributed.barrier()
     K = args.steps
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
+    for e in (x for row in evs for x in row):
+        e.record()  # torch creates the CUDA event lazily, on first record
+    torch.cuda.synchronize()
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     clocks = ClockSampler(local)
     clocks.start()

@@ -1,0 +1,6 @@
+# bench + profiles (one GPU session)
+mkdir -p gpurun_out
+python -m paper_2603_18636_b200.build > gpurun_out/build.log 2>&1 || { cat gpurun_out/build.log; exit 1; }
+timeout 900 python bench.py --steps 5 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"; tail -3 gpurun_out/bench.json; tail -5 gpurun_out/bench.err
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_bsa_fwd -c 1 -o gpurun_out/prof_attn python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_attn.log 2>&1; echo "ncu attn rc=$?"; tail -3 gpurun_out/ncu_attn.log
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_assign -c 2 -o gpurun_out/prof_assign python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_assign.log 2>&1; echo "ncu assign rc=$?"
