@@ -53,7 +53,7 @@ struct Carve {
 };
 
 int round_up(int x, int m) { return (x + m - 1) / m * m; }
-int chunk_n(int ks) { return ks <= 256 ? round_up(ks, 16) : 256; }
+int chunk_n(int ks) { return assign_chunk_n(ks); }
 int pad_k(int ks) {
   const int n = chunk_n(ks);
   return (ks + n - 1) / n * n;
@@ -255,12 +255,15 @@ cs_status run_attn(int B, int H, int N, int d, int kq, int kk, const int32_t* pe
                    cs_bf16_out o, const AttnScratch& sc, cudaStream_t st, void* const* ev = nullptr) {
   const int BH = B * H;
   CS_CUDA(launch_worklist(BH, kq, offs_q, sc.item_start, st), "worklist");
-  CUtensorMap tq, tk, tv;
+  CUtensorMap tq;
+  KVMaps kv;
   CS_CHECK(make_map_2d(&tq, sc.qp, (uint64_t)BH * N, d, 128));
-  CS_CHECK(make_map_2d(&tk, sc.kp, (uint64_t)BH * N, d, 8));
-  CS_CHECK(make_map_2d(&tv, sc.vp, (uint64_t)BH * N, d, 8));
+  for (int i = 0; i < 5; ++i) {
+    CS_CHECK(make_map_2d(&kv.k[i], sc.kp, (uint64_t)BH * N, d, 8u << i));
+    CS_CHECK(make_map_2d(&kv.v[i], sc.vp, (uint64_t)BH * N, d, 8u << i));
+  }
   if (ev) CS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(ev[2]), st), "event");
-  CS_CUDA(launch_bsa_fwd(&tq, &tk, &tv, BH, H, N, d, kq, kk, perm_q, offs_q, offs_k, n_keep, kept,
+  CS_CUDA(launch_bsa_fwd(&tq, &kv, BH, H, N, d, kq, kk, perm_q, offs_q, offs_k, n_keep, kept,
                          sc.item_start, worklist_upper_bound(N, kq), scale,
                          static_cast<__nv_bfloat16*>(o.ptr), o.sb, o.sh, o.sn, st),
           "bsa_fwd");

@@ -44,14 +44,15 @@ struct Smem {
   static constexpr int OFF_KSTART = OFF_MISC + 64;
   static constexpr int OFF_KLEN = OFF_KSTART + kMaxClusters * 4;
   static constexpr int OFF_UCUM = OFF_KLEN + kMaxClusters * 4;
-  static constexpr int BYTES = OFF_UCUM + (kMaxClusters + 1) * 4;
+  static constexpr int OFF_UROW = OFF_UCUM + (kMaxClusters + 1) * 4 + 12;
+  static constexpr int BYTES = OFF_UROW + UPT * 4;
   static constexpr int ALLOC = BYTES + 1024;  // room to align the base to 1024
 };
 
 template <int D>
 __global__ void __launch_bounds__(NTHREADS, 1)
-    k_bsa_fwd(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-              const __grid_constant__ CUtensorMap tm_v, int H, int N, int kq, int kk,
+    k_bsa_fwd(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ KVMaps kv, int H, int N,
+              int kq, int kk,
               const int32_t* __restrict__ perm_q, const int32_t* __restrict__ offs_q,
               const int32_t* __restrict__ offs_k, const int32_t* __restrict__ n_keep,
               const int32_t* __restrict__ kept, const int32_t* __restrict__ item_start,
@@ -72,6 +73,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   int* kstart = reinterpret_cast<int*>(sm + L::OFF_KSTART);
   int* klen = reinterpret_cast<int*>(sm + L::OFF_KLEN);
   int* ucum = reinterpret_cast<int*>(sm + L::OFF_UCUM);
+  int* urow = reinterpret_cast<int*>(sm + L::OFF_UROW);
 
   const int bh = blockIdx.y;
   const int item = blockIdx.x;
@@ -101,7 +103,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   }
   if (warp == WARP_MMA) tmem_alloc(reinterpret_cast<uint32_t*>(misc), 512);
   if (warp == WARP_PRODUCER) {
-    tma_prefetch_desc(&tm_q); tma_prefetch_desc(&tm_k); tma_prefetch_desc(&tm_v);
+    tma_prefetch_desc(&tm_q);
+    if (lane < 5) { tma_prefetch_desc(&kv.k[lane]); tma_prefetch_desc(&kv.v[lane]); }
     const int n = n_keep[bh];
     const int32_t* kl = kept + ((size_t)bh * kq + a) * kk;
     const int32_t* ok = offs_k + (size_t)bh * (kk + 1);
@@ -145,8 +148,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     for (int j = 0; j < nt; ++j) {
       const int stage = j % NST;
       mbar_wait(kv_empty + stage, ((j / NST) & 1) ^ 1);
-      int row = bh * N + kstart[0], valid = 0;
       if (lane < UPT) {
+        int row = bh * N + kstart[0], valid = 0;
         const int g = j * UPT + lane;
         if (g < U) {
           int l2 = 0, h2 = nkeep - 1;
@@ -159,18 +162,32 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           valid = min(UNIT, klen[l2] - u * UNIT);
         }
         vmask[stage * UPT + lane] = (uint8_t)valid;
+        urow[lane] = row;
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive_expect_tx(kv_full + stage, 2 * L::KT);
-      __syncwarp();
-      if (lane < UPT) {
-        for (int hf = 0; hf < L::HALVES; ++hf) {
-          tma_load_2d(sm + L::OFF_K + stage * L::KT + hf * L::HALF_K + lane * 1024, &tm_k, hf * 64,
-                      row, kv_full + stage);
-          tma_load_2d(sm + L::OFF_V + stage * L::KT + hf * L::HALF_K + lane * 1024, &tm_v, hf * 64,
-                      row, kv_full + stage);
+      if (lane == 0) {
+        mbar_arrive_expect_tx(kv_full + stage, 2 * L::KT);
+        // runs of row-contiguous units (the units of one cluster) -> one TMA box per power of two
+        int u = 0;
+        while (u < UPT) {
+          const int r0 = urow[u];
+          int len = 1;
+          while (u + len < UPT && urow[u + len] == r0 + UNIT * len) ++len;
+          int off = 0;
+          for (int bi = 4; bi >= 0; --bi) {
+            if (len & (1 << bi)) {
+              for (int hf = 0; hf < L::HALVES; ++hf) {
+                const uint32_t so = stage * L::KT + hf * L::HALF_K + (u + off) * 1024;
+                tma_load_2d(sm + L::OFF_K + so, &kv.k[bi], hf * 64, r0 + off * UNIT, kv_full + stage);
+                tma_load_2d(sm + L::OFF_V + so, &kv.v[bi], hf * 64, r0 + off * UNIT, kv_full + stage);
+              }
+              off += 1 << bi;
+            }
+          }
+          u += len;
         }
       }
+      __syncwarp();
     }
   } else if (warp == WARP_MMA) {
     // ================= MMA issuer (one thread) =================
@@ -248,15 +265,27 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         tmem_wait_ld();
         mbar_wait(kv_full + stage, (j / NST) & 1);
         const uint4 vw = *reinterpret_cast<const uint4*>(vmask + stage * UPT);
-        float mx = -INFINITY;
+        // mask the rows of partially filled units (the mask is per column: warp-uniform branches)
 #pragma unroll
-        for (int c = 0; c < BN; ++c) {
-          const uint32_t word = (c < 32) ? vw.x : (c < 64) ? vw.y : (c < 96) ? vw.z : vw.w;
-          const uint32_t vcnt = (word >> (8 * ((c >> 3) & 3))) & 0xffu;
-          const float v = ((uint32_t)(c & 7) < vcnt) ? __uint_as_float(su[c]) * scale_log2 : -INFINITY;
-          su[c] = __float_as_uint(v);
-          mx = fmaxf(mx, v);
+        for (int u = 0; u < UPT; ++u) {
+          const uint32_t word = (u < 4) ? vw.x : (u < 8) ? vw.y : (u < 12) ? vw.z : vw.w;
+          const uint32_t vcnt = (word >> (8 * (u & 3))) & 0xffu;
+          if (vcnt < UNIT) {
+#pragma unroll
+            for (int r2 = 0; r2 < UNIT; ++r2)
+              if ((uint32_t)r2 >= vcnt) su[u * UNIT + r2] = 0xff800000u;  // -inf
+          }
         }
+        // row max of the raw scores: 8 independent 3-input max chains
+        float mx8[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) mx8[i] = __uint_as_float(su[i]);
+#pragma unroll
+        for (int c = 8; c < BN; c += 16)
+#pragma unroll
+          for (int i = 0; i < 8; ++i) mx8[i] = fmax3(mx8[i], __uint_as_float(su[c + i]), __uint_as_float(su[c + 8 + i]));
+        const float mx = fmax3(fmax3(mx8[0], mx8[1], mx8[2]), fmax3(mx8[3], mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])) *
+                         scale_log2;
         float alpha = 1.f;
         if (j == 0) {
           m = mx;
@@ -267,14 +296,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
         // tcgen05.ld/st are warp-collective (.sync.aligned): rescale if any row of the warp needs it
         const bool warp_rescale = __any_sync(0xffffffffu, alpha != 1.f);
-        float rs = 0.f;
+        // p = 2^(s*scale_log2 - m): paired FFMA2, MUFU ex2, 4 independent FADD2 row-sum chains
+        const float2 sl2 = make_float2(scale_log2, scale_log2), nm2 = make_float2(-m, -m);
+        float2 acc4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
         for (int c = 0; c < BN; c += 2) {
-          const float p0 = ex2(__uint_as_float(su[c]) - m), p1 = ex2(__uint_as_float(su[c + 1]) - m);
-          rs += p0 + p1;
-          su[c >> 1] = pack_bf16x2(p0, p1);
+          const float2 x = ffma2(make_float2(__uint_as_float(su[c]), __uint_as_float(su[c + 1])), sl2, nm2);
+          const float2 p = make_float2(ex2(x.x), ex2(x.y));
+          acc4[(c >> 1) & 3] = fadd2(acc4[(c >> 1) & 3], p);
+          su[c >> 1] = pack_bf16x2(p.x, p.y);
         }
-        l += rs;
+        const float2 s01 = fadd2(acc4[0], acc4[1]), s23 = fadd2(acc4[2], acc4[3]);
+        const float2 s4 = fadd2(s01, s23);
+        l += s4.x + s4.y;
         tmem_st32(s_tm, su);
         tmem_st32(s_tm + 32, su + 32);
         if (warp_rescale) {  // lazy O rescale; PV(j) is not issued before p_full(j)
@@ -328,7 +362,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
 }  // namespace attn
 
-cudaError_t launch_bsa_fwd(const CUtensorMap* tm_q, const CUtensorMap* tm_k, const CUtensorMap* tm_v,
+cudaError_t launch_bsa_fwd(const CUtensorMap* tm_q, const KVMaps* kv,
                            int BH, int H, int N, int d, int kq, int kk, const int32_t* perm_q,
                            const int32_t* offs_q, const int32_t* offs_k, const int32_t* n_keep,
                            const int32_t* kept, const int32_t* item_start, int items_ub,
@@ -341,14 +375,14 @@ cudaError_t launch_bsa_fwd(const CUtensorMap* tm_q, const CUtensorMap* tm_k, con
     const int smem = attn::Smem<128>::ALLOC;
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    kfn<<<grid, attn::NTHREADS, smem, st>>>(*tm_q, *tm_k, *tm_v, H, N, kq, kk, perm_q, offs_q, offs_k,
+    kfn<<<grid, attn::NTHREADS, smem, st>>>(*tm_q, *kv, H, N, kq, kk, perm_q, offs_q, offs_k,
                                            n_keep, kept, item_start, scale_log2, o, osb, osh, osn);
   } else {
     auto kfn = attn::k_bsa_fwd<64>;
     const int smem = attn::Smem<64>::ALLOC;
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    kfn<<<grid, attn::NTHREADS, smem, st>>>(*tm_q, *tm_k, *tm_v, H, N, kq, kk, perm_q, offs_q, offs_k,
+    kfn<<<grid, attn::NTHREADS, smem, st>>>(*tm_q, *kv, H, N, kq, kk, perm_q, offs_q, offs_k,
                                            n_keep, kept, item_start, scale_log2, o, osb, osh, osn);
   }
   return cudaGetLastError();

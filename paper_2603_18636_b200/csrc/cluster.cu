@@ -103,21 +103,21 @@ __global__ void __launch_bounds__(256) k_init_sample(XView q, XView k, int N, in
 }
 
 // ---------------------------------------------------------------------------------------------
-// a2: Gamma = C_a^T C_a (fp64).  grid (BH, d/16), block 256: rows e in [16 by, 16 by + 16)
+// a2: Gamma = C_a^T C_a (fp64).  grid (BH, d/16), block 256: rows e in [16 by, 16 by + 16).
+// Thread t owns column f = t % d and rows e0 + t/d + EB*i: the staged row r is read along f
+// (conflict-free) and at e (warp-uniform broadcast).
 // ---------------------------------------------------------------------------------------------
 template <int D>
 __global__ void __launch_bounds__(256) k_gamma(const float* __restrict__ ca, int ka,
                                                double* __restrict__ gamma) {
-  constexpr int ROWS = 16, CH = 32, EPT = ROWS * D / 256;
+  constexpr int ROWS = 16, CH = 32, EB = 256 / D, RPT = ROWS / EB;
   __shared__ double sa[CH][D];
   const int bh = blockIdx.x, e0 = blockIdx.y * ROWS;
   const float* A = ca + (size_t)bh * ka * D;
-  const int t = threadIdx.x;
-  const int flat = t * EPT;
-  const int e = e0 + flat / D, f0 = flat % D;
-  double acc[EPT];
+  const int t = threadIdx.x, f = t % D, eb = t / D;
+  double acc[RPT];
 #pragma unroll
-  for (int i = 0; i < EPT; ++i) acc[i] = 0.0;
+  for (int i = 0; i < RPT; ++i) acc[i] = 0.0;
   for (int a0 = 0; a0 < ka; a0 += CH) {
     const int n = min(CH, ka - a0);
     __syncthreads();
@@ -127,91 +127,72 @@ __global__ void __launch_bounds__(256) k_gamma(const float* __restrict__ ca, int
     }
     __syncthreads();
     for (int r = 0; r < n; ++r) {
-      const double ae = sa[r][e];
+      const double vf = sa[r][f];
 #pragma unroll
-      for (int i = 0; i < EPT; ++i) acc[i] = fma(ae, sa[r][f0 + i], acc[i]);
+      for (int i = 0; i < RPT; ++i) acc[i] = fma(sa[r][e0 + eb + EB * i], vf, acc[i]);
     }
   }
-  double* G = gamma + (size_t)bh * D * D + (size_t)e * D + f0;
 #pragma unroll
-  for (int i = 0; i < EPT; ++i) G[i] = acc[i];
+  for (int i = 0; i < RPT; ++i) gamma[(size_t)bh * D * D + (size_t)(e0 + eb + EB * i) * D + f] = acc[i];
 }
 
 // ---------------------------------------------------------------------------------------------
-// a2: W_j = Gamma c_j / ||c_j C_a^T||  ->  Wsplit[bh][j] = [bf16(W) | bf16(W - bf16(W))]
-// grid (ks_pad / 8, BH), block 128.  Rows j >= ks are written as zeros (padding).
+// a2: w_j = Gamma c_j, n_j^2 = ||c_j C_a^T||^2 = c_j . w_j (Gamma = C_a^T C_a),
+//     W_j = w_j / n_j  ->  Wsplit[bh][j] = [bf16(W) | bf16(W - bf16(W))]
+// grid (ks_pad / 32, BH), block 256: 32 centroids per block; thread t owns output column
+// e = t % D for rows j = t / D + EB*i.  Gamma rows are read coalesced along e (Gamma is
+// symmetric).  Rows j >= ks are written as zeros (padding).
 // ---------------------------------------------------------------------------------------------
 template <int D>
-__global__ void __launch_bounds__(128) k_anchor_w(const float* __restrict__ ca, int ka,
-                                                  const float* __restrict__ cs_, int ks, int ks_pad,
+__global__ void __launch_bounds__(256, 1) k_anchor_w(const float* __restrict__ cs_, int ks, int ks_pad,
                                                   const double* __restrict__ gamma,
                                                   __nv_bfloat16* __restrict__ wsplit) {
-  constexpr int J = 8;
+  constexpr int J = 32, EB = 256 / D, RPT = J / EB, WPG = D / 32;  // warps per row group
   __shared__ double sc[J][D];
-  __shared__ double red[J][4];
-  __shared__ double inv_norm[J];
+  __shared__ double red[J][WPG];
   const int bh = blockIdx.y, j0 = blockIdx.x * J, t = threadIdx.x;
-  const float* A = ca + (size_t)bh * ka * D;
+  const int e = t % D, eb = t / D;
   const float* S = cs_ + (size_t)bh * ks * D;
-  for (int i = t; i < J * D; i += 128) {
+  for (int i = t; i < J * D; i += 256) {
     const int r = i / D, c = i % D;
     sc[r][c] = (j0 + r < ks) ? (double)S[(size_t)(j0 + r) * D + c] : 0.0;
   }
   __syncthreads();
-  // ||u_j||^2 with u_j[a] = c_j . C_a[a]
-  double sq[J];
+  const double* G = gamma + (size_t)bh * D * D;
+  double w[RPT];
 #pragma unroll
-  for (int r = 0; r < J; ++r) sq[r] = 0.0;
-  for (int a = t; a < ka; a += 128) {
-    const float* row = A + (size_t)a * D;
-    double u[J];
+  for (int i = 0; i < RPT; ++i) w[i] = 0.0;
+  for (int f = 0; f < D; ++f) {
+    const double g = G[(size_t)f * D + e];
 #pragma unroll
-    for (int r = 0; r < J; ++r) u[r] = 0.0;
-    for (int c = 0; c < D; ++c) {
-      const double v = (double)row[c];
-#pragma unroll
-      for (int r = 0; r < J; ++r) u[r] = fma(v, sc[r][c], u[r]);
-    }
-#pragma unroll
-    for (int r = 0; r < J; ++r) sq[r] = fma(u[r], u[r], sq[r]);
+    for (int i = 0; i < RPT; ++i) w[i] = fma(g, sc[eb + EB * i][f], w[i]);
   }
+  // n_j^2 = sum_e c_j[e] w_j[e]: warp partial sums, combined in a fixed order
 #pragma unroll
-  for (int r = 0; r < J; ++r) {
-    double v = sq[r];
+  for (int i = 0; i < RPT; ++i) {
+    double v = sc[eb + EB * i][e] * w[i];
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if ((t & 31) == 0) red[r][t >> 5] = v;
+    if ((t & 31) == 0) red[eb + EB * i][(t % D) >> 5] = v;
   }
   __syncthreads();
-  if (t < J) {
-    const double n2 = red[t][0] + red[t][1] + red[t][2] + red[t][3];
-    inv_norm[t] = n2 > 0.0 ? 1.0 / sqrt(n2) : 0.0;  // ||Pbar_j|| = 0 -> W_j = 0
-  }
-  __syncthreads();
-  if (t < D) {
-    const double* G = gamma + (size_t)bh * D * D + (size_t)t * D;
-    double w[J];
 #pragma unroll
-    for (int r = 0; r < J; ++r) w[r] = 0.0;
-    for (int f = 0; f < D; ++f) {
-      const double g = G[f];
+  for (int i = 0; i < RPT; ++i) {
+    const int jl = eb + EB * i, j = j0 + jl;
+    if (j >= ks_pad) continue;
+    __nv_bfloat16* out = wsplit + ((size_t)bh * ks_pad + j) * (2 * D);
+    if (j < ks) {
+      double n2 = 0.0;
 #pragma unroll
-      for (int r = 0; r < J; ++r) w[r] = fma(g, sc[r][f], w[r]);
-    }
-#pragma unroll
-    for (int r = 0; r < J; ++r) {
-      const int j = j0 + r;
-      if (j >= ks_pad) break;
-      __nv_bfloat16* out = wsplit + ((size_t)bh * ks_pad + j) * (2 * D);
-      if (j < ks) {
-        const double wv = w[r] * inv_norm[r];
-        const __nv_bfloat16 hi = __double2bfloat16(wv);
-        const __nv_bfloat16 lo = __double2bfloat16(wv - (double)__bfloat162float(hi));
-        out[t] = hi;
-        out[D + t] = lo;
-      } else {
-        out[t] = __float2bfloat16(0.f);
-        out[D + t] = __float2bfloat16(0.f);
-      }
+      for (int q = 0; q < WPG; ++q) n2 += red[jl][q];
+      const double inv = n2 > 0.0 ? 1.0 / sqrt(n2) : 0.0;  // ||Pbar_j|| = 0 -> W_j = 0
+      const double wv = w[i] * inv;
+      const __nv_bfloat16 hi = __double2bfloat16(wv);
+      const __nv_bfloat16 lo = __double2bfloat16(wv - (double)__bfloat162float(hi));
+      out[e] = hi;
+      out[D + e] = lo;
+    } else {
+      out[e] = __float2bfloat16(0.f);
+      out[D + e] = __float2bfloat16(0.f);
     }
   }
 }
@@ -382,10 +363,10 @@ cudaError_t launch_anchor_prep(const float* ca, int ka, const float* cself, int 
                                int BH, int d, double* gamma, __nv_bfloat16* wsplit, cudaStream_t st) {
   if (d == 128) {
     k_gamma<128><<<dim3(BH, 128 / 16), 256, 0, st>>>(ca, ka, gamma);
-    k_anchor_w<128><<<dim3((ks_pad + 7) / 8, BH), 128, 0, st>>>(ca, ka, cself, ks, ks_pad, gamma, wsplit);
+    k_anchor_w<128><<<dim3((ks_pad + 31) / 32, BH), 256, 0, st>>>(cself, ks, ks_pad, gamma, wsplit);
   } else {
     k_gamma<64><<<dim3(BH, 64 / 16), 256, 0, st>>>(ca, ka, gamma);
-    k_anchor_w<64><<<dim3((ks_pad + 7) / 8, BH), 128, 0, st>>>(ca, ka, cself, ks, ks_pad, gamma, wsplit);
+    k_anchor_w<64><<<dim3((ks_pad + 31) / 32, BH), 256, 0, st>>>(cself, ks, ks_pad, gamma, wsplit);
   }
   return cudaGetLastError();
 }

@@ -40,6 +40,7 @@ cudaError_t launch_permute_rows(XView x, int BH, int N, int d, const int32_t* pe
 // ---- assign.cu : labels[bh][n] = argmax_j x_n . W_j  (tcgen05 GEMM + fused argmax epilogue)
 // tm_x: 4D map over x {d, N, H, B} box {64, 128, 1, 1}; tm_w: 2D map over Wsplit {2d, BH*ks_pad}
 // box {64, nch}.
+int assign_chunk_n(int ks);  // centroid columns per TMEM chunk (UMMA N)
 cudaError_t launch_assign_gemm(const CUtensorMap* tm_x, const CUtensorMap* tm_w, int B, int H, int N,
                                int d, int ks, int nch, int ks_pad, int32_t* labels, cudaStream_t st);
 
@@ -54,7 +55,12 @@ cudaError_t launch_worklist(int BH, int kq, const int32_t* offs_q, int32_t* item
 int worklist_upper_bound(int N, int kq);
 
 // ---- attn.cu : block-sparse flash attention over cluster-sorted Q/K/V (bf16 [BH, N, d])
-cudaError_t launch_bsa_fwd(const CUtensorMap* tm_q, const CUtensorMap* tm_k, const CUtensorMap* tm_v,
+// K/V maps over the sorted copies with box heights 8 << i rows (i = 0..4), box width 64 columns
+struct KVMaps {
+  CUtensorMap k[5];
+  CUtensorMap v[5];
+};
+cudaError_t launch_bsa_fwd(const CUtensorMap* tm_q, const KVMaps* kv,
                            int BH, int H, int N, int d, int kq, int kk, const int32_t* perm_q,
                            const int32_t* offs_q, const int32_t* offs_k, const int32_t* n_keep,
                            const int32_t* kept, const int32_t* item_start, int items_ub,

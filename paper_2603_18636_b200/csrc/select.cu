@@ -33,18 +33,22 @@ __global__ void __launch_bounds__(256) k_select_rows(int kq, int kk, int d, cons
   const int32_t* ok = offs_k + (size_t)bh * (kk + 1);
   const int32_t* oq = offs_q + (size_t)bh * (kq + 1);
   const float* crow = cq + ((size_t)bh * kq + a) * d;
-  for (int e = t; e < d; e += 256) scq[e] = (double)crow[e];
-  __syncthreads();
-  for (int j = t; j < P2; j += 256) {
+  (void)scq;
+  // Abar_a = C_q[a] . C_k[j] in fp64: one warp per key centroid, lanes along d (coalesced)
+  const int lane = t & 31, wp = t >> 5;
+  const int vpl = d / 32;  // 4 (d=128) or 2 (d=64)
+  double cqv[4];
+  for (int i = 0; i < vpl; ++i) cqv[i] = (double)crow[lane * vpl + i];
+  for (int j = wp; j < P2; j += 8) {
     double v = -INFINITY;
     if (j < kk && ok[j + 1] - ok[j] > 0) {
-      const float* kr = ck + ((size_t)bh * kk + j) * d;
+      const float* kr = ck + ((size_t)bh * kk + j) * d + lane * vpl;
       double acc = 0.0;
-      for (int e = 0; e < d; ++e) acc = fma(scq[e], (double)kr[e], acc);
+      for (int i = 0; i < vpl; ++i) acc = fma(cqv[i], (double)kr[i], acc);
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
       v = acc;
     }
-    sval[j] = v;
-    sidx[j] = j;
+    if (lane == 0) { sval[j] = v; sidx[j] = j; }
   }
   __syncthreads();
   // bitonic sort: (value desc, index asc)
