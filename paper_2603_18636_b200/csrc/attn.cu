@@ -3,17 +3,20 @@
 //
 // One CTA = one work item (bh, query cluster a, pair of 128-row query tiles of a).  Q/K/V are the
 // cluster-sorted copies [BH, N, d] (bf16).  The kept key clusters of a are packed densely into
-// 128-key tiles made of 16 units of 8 consecutive sorted rows (one TMA box {64 cols, 8 rows} per
-// unit and d-half, landing on one 1024-B SWIZZLE_128B atom), so padding is < 8 rows per kept
-// cluster; rows of a unit past its cluster's end are masked to -inf in the softmax.
+// 128-key tiles made of 16 units of 8 consecutive sorted rows; each run of row-contiguous units
+// (the units of one cluster inside a tile) is fetched with the fewest TMA boxes (heights 8..128
+// rows, one 1 KB SWIZZLE_128B atom per 8 rows), so padding is < 8 rows per kept cluster.  Rows of
+// a cluster's last unit past its end are masked to -inf in the softmax.
 //
 // Warp roles (320 threads):  warps 0-3 softmax/epilogue of Q tile 0 (TMEM lanes 0-127),
 // warps 4-7 the same for Q tile 1, warp 8 TMA producer, warp 9 TMEM allocator + MMA issuer.
 // TMEM (512 cols): S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512); P (bf16x2) overwrites the
 // first 64 columns of its S buffer and feeds the PV MMA from TMEM (A operand), V from SMEM
-// (MN-major).  MMA issue order per KV tile j:  PV0(j), QK0(j+1), PV1(j), QK1(j+1), so the softmax
-// of one tile overlaps the MMAs of the other (FA4-style ping-pong).  Online softmax in the exp2
-// domain with lazy rescaling (only when the running max grows by > 8, i.e. a factor 256).
+// (MN-major).  K and V have separate 2-slot rings: K(j) is released as soon as both QK(j) MMAs
+// complete and V(j) after both PV(j) MMAs, so each is prefetched ~2 tiles ahead.  MMA issue order
+// per KV tile j:  PV0(j), QK0(j+1), PV1(j), QK1(j+1) — the softmax of one Q tile overlaps the
+// MMAs of the other (FA4-style ping-pong).  Online softmax in the exp2 domain with lazy
+// rescaling (only when the running max grows by > 8, i.e. a factor 256).
 // The inverse permutation is fused into the epilogue: row r of the tile is stored as 16-byte
 // vectors to O[b, h, perm_q[p], :] in original token order.
 #include "kernels.cuh"
@@ -37,23 +40,20 @@ struct Smem {
   static constexpr int OFF_K = OFF_Q + 2 * QT;
   static constexpr int OFF_V = OFF_K + NST * KT;
   static constexpr int OFF_BAR = OFF_V + NST * KT;
-  // barriers: q_full, kv_full[NST], kv_empty[NST], s_full[2], p_full[2], o_full  (8 B each)
-  static constexpr int NBAR = 1 + 2 * NST + 2 + 2 + 1;
-  static constexpr int OFF_VMASK = OFF_BAR + 8 * 16;
-  static constexpr int OFF_MISC = OFF_VMASK + NST * UPT;  // tmem slot, U, nt
-  static constexpr int OFF_KSTART = OFF_MISC + 64;
+  // q_full, k_full[2], k_empty[2], v_full[2], v_empty[2], s_full[2], p_full[2], o_full
+  static constexpr int OFF_MISC = OFF_BAR + 8 * 16;  // tmem slot, U, n
+  static constexpr int OFF_UROW = OFF_MISC + 16;      // [NST][UPT] unit start rows
+  static constexpr int OFF_KSTART = OFF_UROW + NST * UPT * 4;
   static constexpr int OFF_KLEN = OFF_KSTART + kMaxClusters * 4;
   static constexpr int OFF_UCUM = OFF_KLEN + kMaxClusters * 4;
-  static constexpr int OFF_UROW = OFF_UCUM + (kMaxClusters + 1) * 4 + 12;
-  static constexpr int BYTES = OFF_UROW + UPT * 4;
+  static constexpr int BYTES = OFF_UCUM + (kMaxClusters + 1) * 4;
   static constexpr int ALLOC = BYTES + 1024;  // room to align the base to 1024
 };
 
 template <int D>
 __global__ void __launch_bounds__(NTHREADS, 1)
     k_bsa_fwd(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ KVMaps kv, int H, int N,
-              int kq, int kk,
-              const int32_t* __restrict__ perm_q, const int32_t* __restrict__ offs_q,
+              int kq, int kk, const int32_t* __restrict__ perm_q, const int32_t* __restrict__ offs_q,
               const int32_t* __restrict__ offs_k, const int32_t* __restrict__ n_keep,
               const int32_t* __restrict__ kept, const int32_t* __restrict__ item_start,
               float scale_log2, __nv_bfloat16* __restrict__ out, long long osb, long long osh,
@@ -63,17 +63,18 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::OFF_BAR);
   uint64_t* q_full = bars;
-  uint64_t* kv_full = bars + 1;
-  uint64_t* kv_empty = bars + 1 + NST;
-  uint64_t* s_full = bars + 1 + 2 * NST;
-  uint64_t* p_full = s_full + 2;
-  uint64_t* o_full = p_full + 2;
-  uint8_t* vmask = sm + L::OFF_VMASK;
+  uint64_t* k_full = bars + 1;
+  uint64_t* k_empty = bars + 3;
+  uint64_t* v_full = bars + 5;
+  uint64_t* v_empty = bars + 7;
+  uint64_t* s_full = bars + 9;
+  uint64_t* p_full = bars + 11;
+  uint64_t* o_full = bars + 13;
   int* misc = reinterpret_cast<int*>(sm + L::OFF_MISC);
+  int* urow = reinterpret_cast<int*>(sm + L::OFF_UROW);
   int* kstart = reinterpret_cast<int*>(sm + L::OFF_KSTART);
   int* klen = reinterpret_cast<int*>(sm + L::OFF_KLEN);
   int* ucum = reinterpret_cast<int*>(sm + L::OFF_UCUM);
-  int* urow = reinterpret_cast<int*>(sm + L::OFF_UROW);
 
   const int bh = blockIdx.y;
   const int item = blockIdx.x;
@@ -96,7 +97,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   // ---- setup: barriers (thread 0), TMEM (warp 9), unit table (warp 8)
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
-    for (int s = 0; s < NST; ++s) { mbar_init(kv_full + s, 1); mbar_init(kv_empty + s, 1); }
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(k_full + s, 1); mbar_init(k_empty + s, 1);
+      mbar_init(v_full + s, 1); mbar_init(v_empty + s, 1);
+    }
     for (int t = 0; t < 2; ++t) { mbar_init(s_full + t, 1); mbar_init(p_full + t, 128); }
     mbar_init(o_full, 1);
     fence_barrier_init();
@@ -136,7 +140,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const int nt = (U + UPT - 1) / UPT;
 
   if (warp == WARP_PRODUCER) {
-    // ================= TMA producer =================
+    // ================= TMA producer: Q, then K(0), {K(j+1), V(j)} =================
     if (lane == 0) {
       const int ntq = has1 ? 2 : 1;
       mbar_arrive_expect_tx(q_full, ntq * L::QT);
@@ -145,49 +149,57 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           tma_load_2d(sm + L::OFF_Q + tq * L::QT + hf * L::HALF_Q, &tm_q, hf * 64,
                       bh * N + qbeg + (t0 + tq) * BM, q_full);
     }
-    for (int j = 0; j < nt; ++j) {
-      const int stage = j % NST;
-      mbar_wait(kv_empty + stage, ((j / NST) & 1) ^ 1);
-      if (lane < UPT) {
-        int row = bh * N + kstart[0], valid = 0;
-        const int g = j * UPT + lane;
-        if (g < U) {
-          int l2 = 0, h2 = nkeep - 1;
-          while (l2 < h2) {
-            const int mid = (l2 + h2 + 1) >> 1;
-            if (ucum[mid] <= g) l2 = mid; else h2 = mid - 1;
+    // issue the TMA boxes of one K or V tile from the unit rows in urow[slot]
+    auto issue_tile = [&](int slot, bool is_v) {
+      uint64_t* bar = (is_v ? v_full : k_full) + slot;
+      uint8_t* base = sm + (is_v ? L::OFF_V : L::OFF_K) + slot * L::KT;
+      const int* ur = urow + slot * UPT;
+      mbar_arrive_expect_tx(bar, L::KT);
+      int u = 0;
+      while (u < UPT) {
+        const int r0 = ur[u];
+        int len = 1;
+        while (u + len < UPT && ur[u + len] == r0 + UNIT * len) ++len;
+        int off = 0;
+        for (int bi = 4; bi >= 0; --bi) {
+          if (len & (1 << bi)) {
+            const CUtensorMap* m = is_v ? &kv.v[bi] : &kv.k[bi];
+            for (int hf = 0; hf < L::HALVES; ++hf)
+              tma_load_2d(base + hf * L::HALF_K + (u + off) * 1024, m, hf * 64, r0 + off * UNIT, bar);
+            off += 1 << bi;
           }
-          const int u = g - ucum[l2];
-          row = bh * N + kstart[l2] + u * UNIT;
-          valid = min(UNIT, klen[l2] - u * UNIT);
         }
-        vmask[stage * UPT + lane] = (uint8_t)valid;
-        urow[lane] = row;
+        u += len;
       }
-      __syncwarp();
-      if (lane == 0) {
-        mbar_arrive_expect_tx(kv_full + stage, 2 * L::KT);
-        // runs of row-contiguous units (the units of one cluster) -> one TMA box per power of two
-        int u = 0;
-        while (u < UPT) {
-          const int r0 = urow[u];
-          int len = 1;
-          while (u + len < UPT && urow[u + len] == r0 + UNIT * len) ++len;
-          int off = 0;
-          for (int bi = 4; bi >= 0; --bi) {
-            if (len & (1 << bi)) {
-              for (int hf = 0; hf < L::HALVES; ++hf) {
-                const uint32_t so = stage * L::KT + hf * L::HALF_K + (u + off) * 1024;
-                tma_load_2d(sm + L::OFF_K + so, &kv.k[bi], hf * 64, r0 + off * UNIT, kv_full + stage);
-                tma_load_2d(sm + L::OFF_V + so, &kv.v[bi], hf * 64, r0 + off * UNIT, kv_full + stage);
-              }
-              off += 1 << bi;
+    };
+    for (int jj = 0; jj <= nt; ++jj) {
+      // K(jj) (one tile ahead of V), then V(jj - 1)
+      if (jj < nt) {
+        const int slot = jj % NST;
+        mbar_wait(k_empty + slot, ((jj / NST) & 1) ^ 1);
+        if (lane < UPT) {
+          int row = bh * N + kstart[0];
+          const int g = jj * UPT + lane;
+          if (g < U) {
+            int l2 = 0, h2 = nkeep - 1;
+            while (l2 < h2) {
+              const int mid = (l2 + h2 + 1) >> 1;
+              if (ucum[mid] <= g) l2 = mid; else h2 = mid - 1;
             }
+            row = bh * N + kstart[l2] + (g - ucum[l2]) * UNIT;
           }
-          u += len;
+          urow[slot * UPT + lane] = row;
         }
+        __syncwarp();
+        if (lane == 0) issue_tile(slot, false);
+        __syncwarp();
       }
-      __syncwarp();
+      if (jj >= 1) {
+        const int j = jj - 1, slot = j % NST;
+        mbar_wait(v_empty + slot, ((j / NST) & 1) ^ 1);
+        if (lane == 0) issue_tile(slot, true);
+        __syncwarp();
+      }
     }
   } else if (warp == WARP_MMA) {
     // ================= MMA issuer (one thread) =================
@@ -196,51 +208,56 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       constexpr uint32_t idesc_pv = idesc_bf16(BM, D, 0, 1);
       const uint32_t sQ = smem_u32(sm + L::OFF_Q), sK = smem_u32(sm + L::OFF_K),
                      sV = smem_u32(sm + L::OFF_V);
-      auto issue_qk = [&](int tq, int stage) {
+      auto issue_qk = [&](int tq, int slot) {
         const uint32_t d_tmem = tmem + tq * 128;
 #pragma unroll
         for (int kk2 = 0; kk2 < D / 16; ++kk2) {
           const uint32_t off = (kk2 >> 2) * L::HALF_Q + (kk2 & 3) * 32;
           const uint32_t offk = (kk2 >> 2) * L::HALF_K + (kk2 & 3) * 32;
           const uint64_t ad = smem_desc_sw128(sQ + tq * L::QT + off, 16, 1024);
-          const uint64_t bd = smem_desc_sw128(sK + stage * L::KT + offk, 16, 1024);
+          const uint64_t bd = smem_desc_sw128(sK + slot * L::KT + offk, 16, 1024);
           mma_ss(d_tmem, ad, bd, idesc_qk, kk2 > 0);
         }
       };
-      auto issue_pv = [&](int tq, int stage, bool acc) {
+      auto issue_pv = [&](int tq, int slot, bool acc) {
         const uint32_t d_tmem = tmem + 256 + tq * 128;
         const uint32_t p_tmem = tmem + tq * 128;
 #pragma unroll
         for (int kk2 = 0; kk2 < BN / 16; ++kk2) {
-          const uint64_t bd = smem_desc_sw128(sV + stage * L::KT + kk2 * 2048, L::HALF_K, 1024);
+          const uint64_t bd = smem_desc_sw128(sV + slot * L::KT + kk2 * 2048, L::HALF_K, 1024);
           mma_ts(d_tmem, p_tmem + kk2 * 8, bd, idesc_pv, (acc || kk2 > 0) ? 1u : 0u);
         }
       };
       mbar_wait(q_full, 0);
-      mbar_wait(kv_full, 0);
+      mbar_wait(k_full, 0);
       tc_fence_after();
       issue_qk(0, 0);
       mma_commit(s_full + 0);
       if (has1) { issue_qk(1, 0); mma_commit(s_full + 1); }
+      mma_commit(k_empty + 0);
       for (int j = 0; j < nt; ++j) {
-        const int stage = j % NST, stage1 = (j + 1) % NST;
+        const int slot = j % NST, slot1 = (j + 1) % NST;
         const bool more = j + 1 < nt;
         mbar_wait(p_full + 0, j & 1);
+        mbar_wait(v_full + slot, (j / NST) & 1);
         tc_fence_after();
-        issue_pv(0, stage, j > 0);
+        issue_pv(0, slot, j > 0);
         if (more) {
-          mbar_wait(kv_full + stage1, ((j + 1) / NST) & 1);
+          mbar_wait(k_full + slot1, ((j + 1) / NST) & 1);
           tc_fence_after();
-          issue_qk(0, stage1);
+          issue_qk(0, slot1);
           mma_commit(s_full + 0);
         }
         if (has1) {
           mbar_wait(p_full + 1, j & 1);
           tc_fence_after();
-          issue_pv(1, stage, j > 0);
+          issue_pv(1, slot, j > 0);
         }
-        mma_commit(kv_empty + stage);
-        if (has1 && more) { issue_qk(1, stage1); mma_commit(s_full + 1); }
+        mma_commit(v_empty + slot);
+        if (more) {
+          if (has1) { issue_qk(1, slot1); mma_commit(s_full + 1); }
+          mma_commit(k_empty + slot1);
+        }
       }
       mma_commit(o_full);
     }
@@ -255,27 +272,48 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const uint32_t s_tm = tmem + lane_off + tq * 128;
       const uint32_t o_tm = tmem + lane_off + 256 + tq * 128;
       float m = -INFINITY, l = 0.f;
+      int ci = 0;  // cursor over kept clusters: the next one whose last unit is not yet masked
       for (int j = 0; j < nt; ++j) {
-        const int stage = j % NST;
         mbar_wait(s_full + tq, j & 1);
         tc_fence_after();
         uint32_t su[BN];
 #pragma unroll
         for (int c = 0; c < BN / 32; ++c) tmem_ld32(s_tm + c * 32, su + c * 32);
-        tmem_wait_ld();
-        mbar_wait(kv_full + stage, (j / NST) & 1);
-        const uint4 vw = *reinterpret_cast<const uint4*>(vmask + stage * UPT);
-        // mask the rows of partially filled units (the mask is per column: warp-uniform branches)
-#pragma unroll
-        for (int u = 0; u < UPT; ++u) {
-          const uint32_t word = (u < 4) ? vw.x : (u < 8) ? vw.y : (u < 12) ? vw.z : vw.w;
-          const uint32_t vcnt = (word >> (8 * (u & 3))) & 0xffu;
-          if (vcnt < UNIT) {
-#pragma unroll
-            for (int r2 = 0; r2 < UNIT; ++r2)
-              if ((uint32_t)r2 >= vcnt) su[u * UNIT + r2] = 0xff800000u;  // -inf
+        // invalid columns of this tile (warp-uniform): rows past each cluster's end in its last
+        // unit, and the padding units after the last kept cluster
+        uint32_t mw0 = 0, mw1 = 0, mw2 = 0, mw3 = 0;
+        const int g0 = j * UPT;
+        while (ci < nkeep) {
+          const int gl = ucum[ci + 1] - 1;  // last unit of kept cluster ci
+          if (gl >= g0 + UPT) break;
+          const int vc = klen[ci] - UNIT * (gl - ucum[ci]);
+          if (vc < UNIT && gl >= ucum[ci]) {
+            const int u = gl - g0;
+            const uint32_t bits = ((0xffu << vc) & 0xffu) << (8 * (u & 3));
+            const int w = u >> 2;
+            mw0 |= w == 0 ? bits : 0u; mw1 |= w == 1 ? bits : 0u;
+            mw2 |= w == 2 ? bits : 0u; mw3 |= w == 3 ? bits : 0u;
+          }
+          ++ci;
+        }
+        if (g0 + UPT > U) {
+          for (int u = U - g0; u < UPT; ++u) {
+            const uint32_t bits = 0xffu << (8 * (u & 3));
+            const int w = u >> 2;
+            mw0 |= w == 0 ? bits : 0u; mw1 |= w == 1 ? bits : 0u;
+            mw2 |= w == 2 ? bits : 0u; mw3 |= w == 3 ? bits : 0u;
           }
         }
+        tmem_wait_ld();
+#define CS_APPLY_MASK(W, MWV)                                                        \
+  if (MWV) {                                                                         \
+    _Pragma("unroll") for (int r2 = 0; r2 < 32; ++r2) if ((MWV >> r2) & 1u) su[W * 32 + r2] = 0xff800000u; \
+  }
+        CS_APPLY_MASK(0, mw0)
+        CS_APPLY_MASK(1, mw1)
+        CS_APPLY_MASK(2, mw2)
+        CS_APPLY_MASK(3, mw3)
+#undef CS_APPLY_MASK
         // row max of the raw scores: 8 independent 3-input max chains
         float mx8[8];
 #pragma unroll
