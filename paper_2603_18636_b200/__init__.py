@@ -20,7 +20,7 @@ __all__ = [
 
 RULE_DENSITY, RULE_AS_WRITTEN, RULE_FIXED = 0, 1, 2
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcoclust.so")
+LIB_PATH = os.environ.get("COCLUST_LIB", os.path.join(_HERE, "libcoclust.so"))
 
 
 class CoclustError(RuntimeError):

@@ -16,14 +16,16 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
-LIB = os.path.join(HERE, "libcoclust.so")
-BUILD = os.path.join(HERE, "_build")
+# variant builds for A/B experiments: CS_VARIANT=name CS_EXTRA_FLAGS="-DFOO" -> libcoclust_name.so
+VARIANT = os.environ.get("CS_VARIANT", "")
+LIB = os.path.join(HERE, f"libcoclust_{VARIANT}.so" if VARIANT else "libcoclust.so")
+BUILD = os.path.join(HERE, f"_build_{VARIANT}" if VARIANT else "_build")
 SOURCES = ["api.cu", "cluster.cu", "assign.cu", "select.cu", "attn.cu"]
 HEADERS = ["common.cuh", "kernels.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
          "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr", "-Xptxas", "-v",
-         "-I", os.path.join(ROOT, "include")]
+         "-I", os.path.join(ROOT, "include")] + os.environ.get("CS_EXTRA_FLAGS", "").split()
 
 
 def _digest(paths):

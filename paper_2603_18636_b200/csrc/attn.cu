@@ -272,7 +272,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const uint32_t s_tm = tmem + lane_off + tq * 128;
       const uint32_t o_tm = tmem + lane_off + 256 + tq * 128;
       float m = -INFINITY, l = 0.f;
-      int ci = 0;  // cursor over kept clusters: the next one whose last unit is not yet masked
+      int ci = 0;
+#ifdef CS_ATTN_DEBUG
+      float dbg_s0_keep = 0.f, dbg_s1_keep = 0.f;
+      uint32_t dbg_mw0_keep = 0;
+#endif  // cursor over kept clusters: the next one whose last unit is not yet masked
       for (int j = 0; j < nt; ++j) {
         mbar_wait(s_full + tq, j & 1);
         tc_fence_after();
@@ -314,12 +318,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         CS_APPLY_MASK(2, mw2)
         CS_APPLY_MASK(3, mw3)
 #undef CS_APPLY_MASK
+#ifdef CS_ATTN_DEBUG
+        if (j == 0) { dbg_s0_keep = __uint_as_float(su[0]); dbg_s1_keep = __uint_as_float(su[1]); dbg_mw0_keep = mw0; }
+#endif
         // row max of the raw scores: 8 independent 3-input max chains
         float mx8[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) mx8[i] = __uint_as_float(su[i]);
+        for (int i = 0; i < 8; ++i) mx8[i] = fmaxf(__uint_as_float(su[i]), __uint_as_float(su[8 + i]));
 #pragma unroll
-        for (int c = 8; c < BN; c += 16)
+        for (int c = 16; c < BN; c += 16)
 #pragma unroll
           for (int i = 0; i < 8; ++i) mx8[i] = fmax3(mx8[i], __uint_as_float(su[c + i]), __uint_as_float(su[c + 8 + i]));
         const float mx = fmax3(fmax3(mx8[0], mx8[1], mx8[2]), fmax3(mx8[3], mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])) *
@@ -339,7 +346,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         float2 acc4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
         for (int c = 0; c < BN; c += 2) {
+#ifdef CS_EXP_OLD
+          const float2 x = make_float2(__uint_as_float(su[c]) * scale_log2 - m, __uint_as_float(su[c + 1]) * scale_log2 - m);
+#else
           const float2 x = ffma2(make_float2(__uint_as_float(su[c]), __uint_as_float(su[c + 1])), sl2, nm2);
+#endif
           const float2 p = make_float2(ex2(x.x), ex2(x.y));
           acc4[(c >> 1) & 3] = fadd2(acc4[(c >> 1) & 3], p);
           su[c >> 1] = pack_bf16x2(p.x, p.y);
@@ -382,6 +393,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
         for (int i = 0; i < 16; ++i)
           pk[i] = pack_bf16x2(__uint_as_float(ov[2 * i]) * inv_l, __uint_as_float(ov[2 * i + 1]) * inv_l);
+#ifdef CS_ATTN_DEBUG
+        if (c == 0) {
+          pk[0] = __float_as_uint(m); pk[1] = __float_as_uint(l); pk[2] = __float_as_uint(dbg_s0_keep);
+          pk[3] = __float_as_uint(dbg_s1_keep); pk[4] = dbg_mw0_keep; pk[5] = (uint32_t)nt; pk[6] = (uint32_t)U;
+          pk[7] = (uint32_t)nkeep;
+        }
+#endif
         if (row_ok) {
           uint4* d4 = reinterpret_cast<uint4*>(dst + c * 32);
 #pragma unroll
