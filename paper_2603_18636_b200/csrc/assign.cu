@@ -44,7 +44,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
              int32_t* __restrict__ labels) {
   using L = Smem<D>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::OFF_BAR);
   uint64_t* x_full = bars;
   uint64_t* x_empty = bars + 2;

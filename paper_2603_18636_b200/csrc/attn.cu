@@ -24,6 +24,15 @@
 namespace cs {
 namespace attn {
 
+#ifdef CS_ATTN_DEBUG
+// event trace of one CTA (blockIdx 0,0): t[event][tile] = clock64 (debug variant only)
+__device__ long long g_trace[16][4096];
+#define CS_TRACE(e, j) \
+  if (blockIdx.x == 0 && blockIdx.y == 0 && (threadIdx.x & 31) == 0 && (j) < 4096) g_trace[e][j] = clock64()
+#else
+#define CS_TRACE(e, j)
+#endif
+
 constexpr int BM = 128, BN = 128, UNIT = 8, UPT = BN / UNIT, NST = 2;
 constexpr int NTHREADS = 320;
 constexpr int WARP_PRODUCER = 8, WARP_MMA = 9;
@@ -60,7 +69,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               long long osn) {
   using L = Smem<D>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // align to 1024 B while keeping the pointer in the shared window (LDS/STS, not generic LD/ST)
+  uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::OFF_BAR);
   uint64_t* q_full = bars;
   uint64_t* k_full = bars + 1;
@@ -71,7 +81,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint64_t* p_full = bars + 11;
   uint64_t* o_full = bars + 13;
   int* misc = reinterpret_cast<int*>(sm + L::OFF_MISC);
-  int* urow = reinterpret_cast<int*>(sm + L::OFF_UROW);
   int* kstart = reinterpret_cast<int*>(sm + L::OFF_KSTART);
   int* klen = reinterpret_cast<int*>(sm + L::OFF_KLEN);
   int* ucum = reinterpret_cast<int*>(sm + L::OFF_UCUM);
@@ -149,56 +158,66 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           tma_load_2d(sm + L::OFF_Q + tq * L::QT + hf * L::HALF_Q, &tm_q, hf * 64,
                       bh * N + qbeg + (t0 + tq) * BM, q_full);
     }
-    // issue the TMA boxes of one K or V tile from the unit rows in urow[slot]
-    auto issue_tile = [&](int slot, bool is_v) {
+    // Unit rows of tile jj, computed by lanes 0..15 (lane u <-> unit u of the tile) with a
+    // cursor over the kept clusters (clusters are visited in order, so each lane walks forward
+    // from the tile's first cluster: usually 0-1 steps).
+    int cur = 0;  // kept-cluster index of the first unit of the current tile (warp-uniform)
+    auto unit_row = [&](int jj) -> int {
+      const int g = jj * UPT + lane;
+      while (cur + 1 < nkeep && ucum[cur + 1] <= jj * UPT) ++cur;
+      int i = cur, row = bh * N + kstart[0];
+      if (lane < UPT && g < U) {
+        while (i + 1 < nkeep && ucum[i + 1] <= g) ++i;
+        row = bh * N + kstart[i] + (g - ucum[i]) * UNIT;
+      }
+      return row;
+    };
+    // Issue one K or V tile: each lane that starts a run of row-contiguous units issues the
+    // power-of-two boxes covering its run (multi-lane TMA issue, no serial walk).
+    auto issue_tile = [&](int slot, bool is_v, int row) {
       uint64_t* bar = (is_v ? v_full : k_full) + slot;
       uint8_t* base = sm + (is_v ? L::OFF_V : L::OFF_K) + slot * L::KT;
-      const int* ur = urow + slot * UPT;
-      mbar_arrive_expect_tx(bar, L::KT);
-      int u = 0;
-      while (u < UPT) {
-        const int r0 = ur[u];
-        int len = 1;
-        while (u + len < UPT && ur[u + len] == r0 + UNIT * len) ++len;
+      const int prev = __shfl_up_sync(0xffffffffu, row, 1);
+      const bool start = lane < UPT && (lane == 0 || row != prev + UNIT);
+      const uint32_t starts = __ballot_sync(0xffffffffu, start) | (1u << UPT);
+      if (lane == 0) mbar_arrive_expect_tx(bar, L::KT);
+      __syncwarp();
+      if (start) {
+        const uint32_t after = starts & ~((2u << lane) - 1u);  // run starts after this lane
+        const int len = __ffs(after) - 1 - lane;
         int off = 0;
+#pragma unroll
         for (int bi = 4; bi >= 0; --bi) {
           if (len & (1 << bi)) {
             const CUtensorMap* m = is_v ? &kv.v[bi] : &kv.k[bi];
+#pragma unroll
             for (int hf = 0; hf < L::HALVES; ++hf)
-              tma_load_2d(base + hf * L::HALF_K + (u + off) * 1024, m, hf * 64, r0 + off * UNIT, bar);
+              tma_load_2d(base + hf * L::HALF_K + (lane + off) * 1024, m, hf * 64, row + off * UNIT, bar);
             off += 1 << bi;
           }
         }
-        u += len;
       }
+      __syncwarp();
     };
+    int row_k = 0, row_v = 0;  // unit rows of the K tile in flight and of the pending V tile
     for (int jj = 0; jj <= nt; ++jj) {
       // K(jj) (one tile ahead of V), then V(jj - 1)
+      const int row_next = jj < nt ? unit_row(jj) : 0;
       if (jj < nt) {
         const int slot = jj % NST;
         mbar_wait(k_empty + slot, ((jj / NST) & 1) ^ 1);
-        if (lane < UPT) {
-          int row = bh * N + kstart[0];
-          const int g = jj * UPT + lane;
-          if (g < U) {
-            int l2 = 0, h2 = nkeep - 1;
-            while (l2 < h2) {
-              const int mid = (l2 + h2 + 1) >> 1;
-              if (ucum[mid] <= g) l2 = mid; else h2 = mid - 1;
-            }
-            row = bh * N + kstart[l2] + (g - ucum[l2]) * UNIT;
-          }
-          urow[slot * UPT + lane] = row;
-        }
-        __syncwarp();
-        if (lane == 0) issue_tile(slot, false);
-        __syncwarp();
+        if (lane == 0) CS_TRACE(9, jj);
+        issue_tile(slot, false, row_next);
+        if (lane == 0) CS_TRACE(0, jj);
       }
+      row_v = row_k;
+      row_k = row_next;
       if (jj >= 1) {
         const int j = jj - 1, slot = j % NST;
         mbar_wait(v_empty + slot, ((j / NST) & 1) ^ 1);
-        if (lane == 0) issue_tile(slot, true);
-        __syncwarp();
+        if (lane == 0) CS_TRACE(10, j);
+        issue_tile(slot, true, row_v);
+        if (lane == 0) CS_TRACE(1, j);
       }
     }
   } else if (warp == WARP_MMA) {
@@ -239,17 +258,21 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const int slot = j % NST, slot1 = (j + 1) % NST;
         const bool more = j + 1 < nt;
         mbar_wait(p_full + 0, j & 1);
+        CS_TRACE(4, j);
         mbar_wait(v_full + slot, (j / NST) & 1);
+        CS_TRACE(3, j);
         tc_fence_after();
         issue_pv(0, slot, j > 0);
         if (more) {
           mbar_wait(k_full + slot1, ((j + 1) / NST) & 1);
+          CS_TRACE(2, j + 1);
           tc_fence_after();
           issue_qk(0, slot1);
           mma_commit(s_full + 0);
         }
         if (has1) {
           mbar_wait(p_full + 1, j & 1);
+          CS_TRACE(11, j);
           tc_fence_after();
           issue_pv(1, slot, j > 0);
         }
@@ -279,6 +302,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #endif  // cursor over kept clusters: the next one whose last unit is not yet masked
       for (int j = 0; j < nt; ++j) {
         mbar_wait(s_full + tq, j & 1);
+        CS_TRACE(5 + 2 * tq, j);
         tc_fence_after();
         uint32_t su[BN];
 #pragma unroll
@@ -331,6 +355,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           for (int i = 0; i < 8; ++i) mx8[i] = fmax3(mx8[i], __uint_as_float(su[c + i]), __uint_as_float(su[c + 8 + i]));
         const float mx = fmax3(fmax3(mx8[0], mx8[1], mx8[2]), fmax3(mx8[3], mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])) *
                          scale_log2;
+        CS_TRACE(12 + tq, j);
         float alpha = 1.f;
         if (j == 0) {
           m = mx;
@@ -351,13 +376,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #else
           const float2 x = ffma2(make_float2(__uint_as_float(su[c]), __uint_as_float(su[c + 1])), sl2, nm2);
 #endif
-          const float2 p = make_float2(ex2(x.x), ex2(x.y));
+          // every 4th pair on the FMA pipe (polynomial), the rest on MUFU: keeps MUFU below the
+          // tensor-core time of the two ping-ponged tiles
+          const float2 p = ((c >> 1) & 3) == 3 ? ex2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
           acc4[(c >> 1) & 3] = fadd2(acc4[(c >> 1) & 3], p);
           su[c >> 1] = pack_bf16x2(p.x, p.y);
         }
         const float2 s01 = fadd2(acc4[0], acc4[1]), s23 = fadd2(acc4[2], acc4[3]);
         const float2 s4 = fadd2(s01, s23);
         l += s4.x + s4.y;
+        CS_TRACE(14 + tq, j);
         tmem_st32(s_tm, su);
         tmem_st32(s_tm + 32, su + 32);
         if (warp_rescale) {  // lazy O rescale; PV(j) is not issued before p_full(j)
@@ -374,6 +402,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(p_full + tq);
+        CS_TRACE(6 + 2 * tq, j);
       }
       // ---- epilogue: O / l -> bf16, scattered to original token order
       mbar_wait(o_full, 0);
@@ -417,6 +446,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 }
 
 }  // namespace attn
+
+#ifdef CS_ATTN_DEBUG
+extern "C" int cs_debug_attn_trace(void* host, size_t bytes) {
+  return (int)cudaMemcpyFromSymbol(host, attn::g_trace, bytes < sizeof(attn::g_trace) ? bytes : sizeof(attn::g_trace));
+}
+#endif
 
 cudaError_t launch_bsa_fwd(const CUtensorMap* tm_q, const KVMaps* kv,
                            int BH, int H, int N, int d, int kq, int kk, const int32_t* perm_q,

@@ -216,6 +216,24 @@ CS_DEV float2 fadd2(float2 a, float2 b) {
   return bits_f2(d);
 }
 
+// 2^x for a pair of x <= 0 on the FMA pipe (offloads MUFU.EX2): round-to-nearest split
+// x = j + f, f in [-1/2, 1/2], 2^f by a degree-3 polynomial (max rel. error 7.7e-5, far below the
+// bf16 rounding of P), exponent added in the integer domain.  x is clamped to >= -126 so the
+// exponent add cannot underflow (2^-126 is below every other term of a softmax row sum).
+CS_DEV float2 ex2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -126.f);
+  x.y = fmaxf(x.y, -126.f);
+  const float2 magic = make_float2(12582912.f, 12582912.f);  // 1.5 * 2^23
+  const float2 t = fadd2(x, magic);                           // low mantissa bits hold round(x)
+  const float2 jf = fadd2(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = fadd2(x, make_float2(-jf.x, -jf.y));
+  float2 p = ffma2(make_float2(0.05508876703f, 0.05508876703f), f, make_float2(0.2426046559f, 0.2426046559f));
+  p = ffma2(p, f, make_float2(0.6932762833f, 0.6932762833f));
+  p = ffma2(p, f, make_float2(0.9999289048f, 0.9999289048f));
+  const int ex = __float_as_int(t.x) << 23, ey = __float_as_int(t.y) << 23;
+  return make_float2(__int_as_float(__float_as_int(p.x) + ex), __int_as_float(__float_as_int(p.y) + ey));
+}
+
 template <typename T>
 CS_DEV T warp_sum(T v) {
 #pragma unroll
