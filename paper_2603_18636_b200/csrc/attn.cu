@@ -26,7 +26,7 @@ namespace attn {
 
 #ifdef CS_ATTN_DEBUG
 // event trace of one CTA (blockIdx 0,0): t[event][tile] = clock64 (debug variant only)
-__device__ long long g_trace[16][4096];
+__device__ long long g_trace[20][4096];
 #define CS_TRACE(e, j) \
   if (blockIdx.x == 0 && blockIdx.y == 0 && (threadIdx.x & 31) == 0 && (j) < 4096) g_trace[e][j] = clock64()
 #else
@@ -37,6 +37,10 @@ constexpr int BM = 128, BN = 128, UNIT = 8, UPT = BN / UNIT, NST = 2;
 constexpr int NTHREADS = 320;
 constexpr int WARP_PRODUCER = 8, WARP_MMA = 9;
 constexpr float kRescaleThresh = 8.0f;
+#ifndef CS_POLY_EVERY
+#define CS_POLY_EVERY 4
+#endif
+constexpr int kPolyEvery = CS_POLY_EVERY;  // one exp2 pair in kPolyEvery on the FMA pipe (0: none)
 
 template <int D>
 struct Smem {
@@ -295,21 +299,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const uint32_t s_tm = tmem + lane_off + tq * 128;
       const uint32_t o_tm = tmem + lane_off + 256 + tq * 128;
       float m = -INFINITY, l = 0.f;
-      int ci = 0;
-#ifdef CS_ATTN_DEBUG
-      float dbg_s0_keep = 0.f, dbg_s1_keep = 0.f;
-      uint32_t dbg_mw0_keep = 0;
-#endif  // cursor over kept clusters: the next one whose last unit is not yet masked
-      for (int j = 0; j < nt; ++j) {
-        mbar_wait(s_full + tq, j & 1);
-        CS_TRACE(5 + 2 * tq, j);
-        tc_fence_after();
-        uint32_t su[BN];
-#pragma unroll
-        for (int c = 0; c < BN / 32; ++c) tmem_ld32(s_tm + c * 32, su + c * 32);
-        // invalid columns of this tile (warp-uniform): rows past each cluster's end in its last
-        // unit, and the padding units after the last kept cluster
-        uint32_t mw0 = 0, mw1 = 0, mw2 = 0, mw3 = 0;
+      // invalid columns of tile j (warp-uniform): rows past each kept cluster's end in its last
+      // unit, and the padding units after the last kept cluster.  Computed one tile ahead, while
+      // the warp waits for the next S, so it is off the softmax critical path.
+      int ci = 0;  // cursor over kept clusters: the next one whose last unit is not yet masked
+      uint32_t mw0 = 0, mw1 = 0, mw2 = 0, mw3 = 0;
+      auto tile_mask = [&](int j) {
+        mw0 = mw1 = mw2 = mw3 = 0;
         const int g0 = j * UPT;
         while (ci < nkeep) {
           const int gl = ucum[ci + 1] - 1;  // last unit of kept cluster ci
@@ -332,6 +328,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             mw2 |= w == 2 ? bits : 0u; mw3 |= w == 3 ? bits : 0u;
           }
         }
+      };
+#ifdef CS_ATTN_DEBUG
+      float dbg_s0_keep = 0.f, dbg_s1_keep = 0.f;
+      uint32_t dbg_mw0_keep = 0;
+#endif
+      tile_mask(0);
+      for (int j = 0; j < nt; ++j) {
+        mbar_wait(s_full + tq, j & 1);
+        CS_TRACE(5 + 2 * tq, j);
+        tc_fence_after();
+        uint32_t su[BN];
+#pragma unroll
+        for (int c = 0; c < BN / 32; ++c) tmem_ld32(s_tm + c * 32, su + c * 32);
         tmem_wait_ld();
 #define CS_APPLY_MASK(W, MWV)                                                        \
   if (MWV) {                                                                         \
@@ -345,6 +354,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #ifdef CS_ATTN_DEBUG
         if (j == 0) { dbg_s0_keep = __uint_as_float(su[0]); dbg_s1_keep = __uint_as_float(su[1]); dbg_mw0_keep = mw0; }
 #endif
+        CS_TRACE(16 + tq, j);
         // row max of the raw scores: 8 independent 3-input max chains
         float mx8[8];
 #pragma unroll
@@ -378,7 +388,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #endif
           // every 4th pair on the FMA pipe (polynomial), the rest on MUFU: keeps MUFU below the
           // tensor-core time of the two ping-ponged tiles
-          const float2 p = ((c >> 1) & 3) == 3 ? ex2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
+          const float2 p = (kPolyEvery > 0 && ((c >> 1) % kPolyEvery) == kPolyEvery - 1)
+                               ? ex2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
           acc4[(c >> 1) & 3] = fadd2(acc4[(c >> 1) & 3], p);
           su[c >> 1] = pack_bf16x2(p.x, p.y);
         }
@@ -403,6 +414,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         tc_fence_before();
         mbar_arrive(p_full + tq);
         CS_TRACE(6 + 2 * tq, j);
+        if (j + 1 < nt) tile_mask(j + 1);
       }
       // ---- epilogue: O / l -> bf16, scattered to original token order
       mbar_wait(o_full, 0);

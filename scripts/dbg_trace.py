@@ -10,7 +10,7 @@ budget = torch.full((H,), 0.2, device='cuda')
 for _ in range(2):
     o = pb.coclust_sparse_attention(w.q, w.k, w.v, 100, 500, 2, budget, rule=pb.RULE_FIXED)
 torch.cuda.synchronize()
-buf = np.zeros((16, 4096), np.int64)
+buf = np.zeros((20, 4096), np.int64)
 L = pb.lib()
 L.cs_debug_attn_trace.restype = ctypes.c_int
 rc = L.cs_debug_attn_trace(buf.ctypes.data_as(ctypes.c_void_p), ctypes.c_size_t(buf.nbytes))
@@ -31,4 +31,5 @@ print('K issued(j) -> M:k_full(j) median', np.median(buf[2, 2:nt] - buf[0, 2:nt]
 
 print('K: k_empty wait done -> issued', np.median(buf[0, 2:nt] - buf[9, 2:nt]), ' prev V issued -> k_empty done', np.median(buf[9, 2:nt] - buf[1, 1:nt-1]))
 print('V: v_empty wait done -> issued', np.median(buf[1, 2:nt] - buf[10, 2:nt]), ' K issued -> v_empty done', np.median(buf[10, 2:nt] - buf[0, 3:nt+1]))
+print('softmax0: s_full->masked', np.median(buf[16, 1:nt] - buf[5, 1:nt]), 'masked->max', np.median(buf[12, 1:nt] - buf[16, 1:nt]))
 print('softmax0: s_full->max', np.median(buf[12, 1:nt] - buf[5, 1:nt]), 'max->exp done', np.median(buf[14, 1:nt] - buf[12, 1:nt]), 'exp done->arrive', np.median(buf[6, 1:nt] - buf[14, 1:nt]))
