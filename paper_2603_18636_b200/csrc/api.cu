@@ -258,7 +258,7 @@ cs_status run_attn(int B, int H, int N, int d, int kq, int kk, const int32_t* pe
   CUtensorMap tq;
   KVMaps kv;
   CS_CHECK(make_map_2d(&tq, sc.qp, (uint64_t)BH * N, d, 128));
-  for (int i = 0; i < 4; ++i) {  // box heights 8..64 rows (64-key tiles)
+  for (int i = 0; i < 5; ++i) {  // box heights 8..128 rows
     CS_CHECK(make_map_2d(&kv.k[i], sc.kp, (uint64_t)BH * N, d, 8u << i));
     CS_CHECK(make_map_2d(&kv.v[i], sc.vp, (uint64_t)BH * N, d, 8u << i));
   }

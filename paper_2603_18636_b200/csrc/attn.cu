@@ -3,25 +3,22 @@
 //
 // One CTA = one work item (bh, query cluster a, pair of 128-row query tiles of a).  Q/K/V are the
 // cluster-sorted copies [BH, N, d] (bf16).  The kept key clusters of a are packed densely into
-// 64-key tiles made of 8 units of 8 consecutive sorted rows; each run of row-contiguous units (the
-// units of one cluster inside a tile) is fetched with the fewest TMA boxes (heights 8..64 rows, one
-// 1 KB SWIZZLE_128B atom per 8 rows), so padding is < 8 rows per kept cluster.  Rows of a
-// cluster's last unit past its end are masked to -inf in the softmax.
+// 128-key tiles made of 16 units of 8 consecutive sorted rows; each run of row-contiguous units
+// (the units of one cluster inside a tile) is fetched with the fewest TMA boxes (heights 8..128
+// rows, one 1 KB SWIZZLE_128B atom per 8 rows), so padding is < 8 rows per kept cluster.  Rows of
+// a cluster's last unit past its end are masked to -inf in the softmax.
 //
-// Warp roles (320 threads): warps 0-3 softmax/epilogue of Q tile 0 (TMEM lanes 0-127), warps 4-7
-// the same for Q tile 1, warp 8 TMA producer, warp 9 TMEM allocator + MMA issuer.
-// TMEM (512 columns): S[t][b] = (2t+b)*64 (two 64-column score buffers per Q tile t), O[t] =
-// 256 + 128t.  P (bf16x2, 32 columns) overwrites the first half of its own S buffer and feeds the
-// PV MMA from TMEM (A operand); V comes from SMEM (MN-major).
-// Because S is double buffered, QK(j+1) never waits for softmax(j): the MMA issue order is
-//     QK0(j+1), QK1(j+1), PV0(j), PV1(j), QK0(j+2), ...
-// so the softmax warps run tile after tile while the tensor core computes the next scores, and
-// the only coupling is PV(j) <- P(j).  Per 64-key step the tensor core does 4 x 256 cycles and each
-// SMSP's two softmax warps do 2 x 64 exp2 per lane; a fraction of the exp2 runs as a polynomial on
-// the FMA pipe so MUFU is not the co-bottleneck.
-// Online softmax in the exp2 domain with lazy rescaling (only when the running max grows by > 8);
-// a rescale waits for the previous PV of its tile (o_ready barrier) before touching O in TMEM.
-// K and V have separate 4-slot rings.  The inverse permutation is fused into the epilogue stores.
+// Warp roles (320 threads):  warps 0-3 softmax/epilogue of Q tile 0 (TMEM lanes 0-127),
+// warps 4-7 the same for Q tile 1, warp 8 TMA producer, warp 9 TMEM allocator + MMA issuer.
+// TMEM (512 cols): S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512); P (bf16x2) overwrites the
+// first 64 columns of its S buffer and feeds the PV MMA from TMEM (A operand), V from SMEM
+// (MN-major).  K and V have separate 2-slot rings: K(j) is released as soon as both QK(j) MMAs
+// complete and V(j) after both PV(j) MMAs, so each is prefetched ~2 tiles ahead.  MMA issue order
+// per KV tile j:  PV0(j), QK0(j+1), PV1(j), QK1(j+1) — the softmax of one Q tile overlaps the
+// MMAs of the other (FA4-style ping-pong).  Online softmax in the exp2 domain with lazy
+// rescaling (only when the running max grows by > 8, i.e. a factor 256).
+// The inverse permutation is fused into the epilogue: row r of the tile is stored as 16-byte
+// vectors to O[b, h, perm_q[p], :] in original token order.
 #include "kernels.cuh"
 
 namespace cs {
@@ -36,9 +33,9 @@ __device__ long long g_trace[20][4096];
 #define CS_TRACE(e, j)
 #endif
 
-constexpr int BM = 128, BN = 64, UNIT = 8, UPT = BN / UNIT, NSK = 4, NSV = 4;
-constexpr int NTHREADS = 320;
-constexpr int WARP_PRODUCER = 8, WARP_MMA = 9;
+constexpr int BM = 128, BN = 128, UNIT = 8, UPT = BN / UNIT, NST = 2;
+constexpr int NTHREADS = 352;
+constexpr int WARP_PRODUCER = 8, WARP_MMA = 9, WARP_VLOAD = 10;
 constexpr float kRescaleThresh = 8.0f;
 #ifndef CS_POLY_EVERY
 #define CS_POLY_EVERY 4
@@ -54,12 +51,12 @@ struct Smem {
   static constexpr int HALF_K = BN * 128;
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_K = OFF_Q + 2 * QT;
-  static constexpr int OFF_V = OFF_K + NSK * KT;
-  static constexpr int OFF_BAR = OFF_V + NSV * KT;
-  // q_full, k_full[4], k_empty[4], v_full[4], v_empty[4], s_full[2][2], p_full[2][2],
-  // o_ready[2], o_full  (8 B each, 28 used)
-  static constexpr int OFF_MISC = OFF_BAR + 8 * 32;  // tmem slot, U, n
-  static constexpr int OFF_KSTART = OFF_MISC + 16;
+  static constexpr int OFF_V = OFF_K + NST * KT;
+  static constexpr int OFF_BAR = OFF_V + NST * KT;
+  // q_full, k_full[2], k_empty[2], v_full[2], v_empty[2], s_full[2], p_full[2], o_full
+  static constexpr int OFF_MISC = OFF_BAR + 8 * 16;  // tmem slot, U, n
+  static constexpr int OFF_UROW = OFF_MISC + 16;      // [NST][UPT] unit start rows
+  static constexpr int OFF_KSTART = OFF_UROW + NST * UPT * 4;
   static constexpr int OFF_KLEN = OFF_KSTART + kMaxClusters * 4;
   static constexpr int OFF_UCUM = OFF_KLEN + kMaxClusters * 4;
   static constexpr int BYTES = OFF_UCUM + (kMaxClusters + 1) * 4;
@@ -81,13 +78,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::OFF_BAR);
   uint64_t* q_full = bars;
   uint64_t* k_full = bars + 1;
-  uint64_t* k_empty = bars + 5;
-  uint64_t* v_full = bars + 9;
-  uint64_t* v_empty = bars + 13;
-  uint64_t* s_full = bars + 17;   // [t*2 + b]
-  uint64_t* p_full = bars + 21;   // [t*2 + b]
-  uint64_t* o_ready = bars + 25;  // [t]
-  uint64_t* o_full = bars + 27;
+  uint64_t* k_empty = bars + 3;
+  uint64_t* v_full = bars + 5;
+  uint64_t* v_empty = bars + 7;
+  uint64_t* s_full = bars + 9;
+  uint64_t* p_full = bars + 11;
+  uint64_t* o_full = bars + 13;
   int* misc = reinterpret_cast<int*>(sm + L::OFF_MISC);
   int* kstart = reinterpret_cast<int*>(sm + L::OFF_KSTART);
   int* klen = reinterpret_cast<int*>(sm + L::OFF_KLEN);
@@ -114,17 +110,18 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   // ---- setup: barriers (thread 0), TMEM (warp 9), unit table (warp 8)
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
-    for (int s = 0; s < NSK; ++s) { mbar_init(k_full + s, 1); mbar_init(k_empty + s, 1); }
-    for (int s = 0; s < NSV; ++s) { mbar_init(v_full + s, 1); mbar_init(v_empty + s, 1); }
-    for (int i = 0; i < 4; ++i) { mbar_init(s_full + i, 1); mbar_init(p_full + i, 128); }
-    for (int t = 0; t < 2; ++t) mbar_init(o_ready + t, 1);
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(k_full + s, 1); mbar_init(k_empty + s, 1);
+      mbar_init(v_full + s, 1); mbar_init(v_empty + s, 1);
+    }
+    for (int t = 0; t < 2; ++t) { mbar_init(s_full + t, 1); mbar_init(p_full + t, 128); }
     mbar_init(o_full, 1);
     fence_barrier_init();
   }
   if (warp == WARP_MMA) tmem_alloc(reinterpret_cast<uint32_t*>(misc), 512);
   if (warp == WARP_PRODUCER) {
     tma_prefetch_desc(&tm_q);
-    if (lane < 4) { tma_prefetch_desc(&kv.k[lane]); tma_prefetch_desc(&kv.v[lane]); }
+    if (lane < 5) { tma_prefetch_desc(&kv.k[lane]); tma_prefetch_desc(&kv.v[lane]); }
     const int n = n_keep[bh];
     const int32_t* kl = kept + ((size_t)bh * kq + a) * kk;
     const int32_t* ok = offs_k + (size_t)bh * (kk + 1);
@@ -155,9 +152,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const int nkeep = misc[2];
   const int nt = (U + UPT - 1) / UPT;
 
-  if (warp == WARP_PRODUCER) {
-    // ================= TMA producer: Q, then K(0), {K(j+1), V(j)} =================
-    if (lane == 0) {
+  if (warp == WARP_PRODUCER || warp == WARP_VLOAD) {
+    // ================= TMA producers: warp 8 -> Q and K(j), warp 10 -> V(j) =================
+    const bool is_v = warp == WARP_VLOAD;
+    if (!is_v && lane == 0) {
       const int ntq = has1 ? 2 : 1;
       mbar_arrive_expect_tx(q_full, ntq * L::QT);
       for (int tq = 0; tq < ntq; ++tq)
@@ -180,7 +178,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     };
     // Issue one K or V tile: each lane that starts a run of row-contiguous units issues the
     // power-of-two boxes covering its run (multi-lane TMA issue).
-    auto issue_tile = [&](uint64_t* bar, uint8_t* base, bool is_v, int row) {
+    auto issue_tile = [&](uint64_t* bar, uint8_t* base, int row) {
       const int prev = __shfl_up_sync(0xffffffffu, row, 1);
       const bool start = lane < UPT && (lane == 0 || row != prev + UNIT);
       const uint32_t starts = __ballot_sync(0xffffffffu, start) | (1u << UPT);
@@ -191,7 +189,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const int len = __ffs(after) - 1 - lane;
         int off = 0;
 #pragma unroll
-        for (int bi = 3; bi >= 0; --bi) {
+        for (int bi = 4; bi >= 0; --bi) {
           if (len & (1 << bi)) {
             const CUtensorMap* m = is_v ? &kv.v[bi] : &kv.k[bi];
 #pragma unroll
@@ -203,26 +201,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
       __syncwarp();
     };
-    int rows0 = 0, rows1 = 0, rows2 = 0, rows3 = 0;  // unit rows of the last NSK K tiles
-    for (int jj = 0; jj <= nt; ++jj) {
-      if (jj < nt) {
-        const int slot = jj % NSK;
-        const int row = unit_row(jj);
-        mbar_wait(k_empty + slot, ((jj / NSK) & 1) ^ 1);
-        if (lane == 0) CS_TRACE(9, jj);
-        issue_tile(k_full + slot, sm + L::OFF_K + slot * L::KT, false, row);
-        if (lane == 0) CS_TRACE(0, jj);
-        rows0 = slot == 0 ? row : rows0; rows1 = slot == 1 ? row : rows1;
-        rows2 = slot == 2 ? row : rows2; rows3 = slot == 3 ? row : rows3;
-      }
-      if (jj >= 1) {
-        const int j = jj - 1, slot = j % NSV, ks = j % NSK;  // V(j) reuses K(j)'s unit rows
-        const int row = ks == 0 ? rows0 : ks == 1 ? rows1 : ks == 2 ? rows2 : rows3;
-        mbar_wait(v_empty + slot, ((j / NSV) & 1) ^ 1);
-        if (lane == 0) CS_TRACE(10, j);
-        issue_tile(v_full + slot, sm + L::OFF_V + slot * L::KT, true, row);
-        if (lane == 0) CS_TRACE(1, j);
-      }
+    uint64_t* full = is_v ? v_full : k_full;
+    uint64_t* empty = is_v ? v_empty : k_empty;
+    uint8_t* ring = sm + (is_v ? L::OFF_V : L::OFF_K);
+    for (int jj = 0; jj < nt; ++jj) {
+      const int slot = jj % NST;
+      const int row = unit_row(jj);
+      mbar_wait(empty + slot, ((jj / NST) & 1) ^ 1);
+      if (lane == 0) CS_TRACE(is_v ? 10 : 9, jj);
+      issue_tile(full + slot, ring + slot * L::KT, row);
+      if (lane == 0) CS_TRACE(is_v ? 1 : 0, jj);
     }
   } else if (warp == WARP_MMA) {
     // ================= MMA issuer (one thread) =================
@@ -231,53 +219,60 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       constexpr uint32_t idesc_pv = idesc_bf16(BM, D, 0, 1);
       const uint32_t sQ = smem_u32(sm + L::OFF_Q), sK = smem_u32(sm + L::OFF_K),
                      sV = smem_u32(sm + L::OFF_V);
-      const int ntq = has1 ? 2 : 1;
-      auto issue_qk = [&](int tq, int j) {
-        const uint32_t d_tmem = tmem + (tq * 2 + (j & 1)) * 64;
-        const uint32_t kb = sK + (j % NSK) * L::KT;
+      auto issue_qk = [&](int tq, int slot) {
+        const uint32_t d_tmem = tmem + tq * 128;
 #pragma unroll
         for (int kk2 = 0; kk2 < D / 16; ++kk2) {
           const uint32_t off = (kk2 >> 2) * L::HALF_Q + (kk2 & 3) * 32;
           const uint32_t offk = (kk2 >> 2) * L::HALF_K + (kk2 & 3) * 32;
           const uint64_t ad = smem_desc_sw128(sQ + tq * L::QT + off, 16, 1024);
-          const uint64_t bd = smem_desc_sw128(kb + offk, 16, 1024);
+          const uint64_t bd = smem_desc_sw128(sK + slot * L::KT + offk, 16, 1024);
           mma_ss(d_tmem, ad, bd, idesc_qk, kk2 > 0);
         }
       };
-      auto issue_pv = [&](int tq, int j) {
+      auto issue_pv = [&](int tq, int slot, bool acc) {
         const uint32_t d_tmem = tmem + 256 + tq * 128;
-        const uint32_t p_tmem = tmem + (tq * 2 + (j & 1)) * 64;
-        const uint32_t vb = sV + (j % NSV) * L::KT;
+        const uint32_t p_tmem = tmem + tq * 128;
 #pragma unroll
         for (int kk2 = 0; kk2 < BN / 16; ++kk2) {
-          const uint64_t bd = smem_desc_sw128(vb + kk2 * 2048, L::HALF_K, 1024);
-          mma_ts(d_tmem, p_tmem + kk2 * 8, bd, idesc_pv, (j > 0 || kk2 > 0) ? 1u : 0u);
+          const uint64_t bd = smem_desc_sw128(sV + slot * L::KT + kk2 * 2048, L::HALF_K, 1024);
+          mma_ts(d_tmem, p_tmem + kk2 * 8, bd, idesc_pv, (acc || kk2 > 0) ? 1u : 0u);
         }
-      };
-      auto qk_step = [&](int j) {  // QK(j) for both Q tiles into S[.][j&1]
-        mbar_wait(k_full + j % NSK, (j / NSK) & 1);
-        tc_fence_after();
-        CS_TRACE(2, j);
-        for (int tq = 0; tq < ntq; ++tq) {
-          issue_qk(tq, j);
-          mma_commit(s_full + tq * 2 + (j & 1));
-        }
-        mma_commit(k_empty + j % NSK);
       };
       mbar_wait(q_full, 0);
-      qk_step(0);
+      mbar_wait(k_full, 0);
+      tc_fence_after();
+      issue_qk(0, 0);
+      mma_commit(s_full + 0);
+      if (has1) { issue_qk(1, 0); mma_commit(s_full + 1); }
+      mma_commit(k_empty + 0);
       for (int j = 0; j < nt; ++j) {
-        if (j + 1 < nt) qk_step(j + 1);  // S[.][(j+1)&1] is free: PV(j-1) was issued before
-        mbar_wait(v_full + j % NSV, (j / NSV) & 1);
+        const int slot = j % NST, slot1 = (j + 1) % NST;
+        const bool more = j + 1 < nt;
+        mbar_wait(p_full + 0, j & 1);
+        CS_TRACE(4, j);
+        mbar_wait(v_full + slot, (j / NST) & 1);
         CS_TRACE(3, j);
-        for (int tq = 0; tq < ntq; ++tq) {
-          mbar_wait(p_full + tq * 2 + (j & 1), (j >> 1) & 1);
+        tc_fence_after();
+        issue_pv(0, slot, j > 0);
+        if (more) {
+          mbar_wait(k_full + slot1, ((j + 1) / NST) & 1);
+          CS_TRACE(2, j + 1);
           tc_fence_after();
-          CS_TRACE(4 + 7 * tq, j);
-          issue_pv(tq, j);
-          mma_commit(o_ready + tq);
+          issue_qk(0, slot1);
+          mma_commit(s_full + 0);
         }
-        mma_commit(v_empty + j % NSV);
+        if (has1) {
+          mbar_wait(p_full + 1, j & 1);
+          CS_TRACE(11, j);
+          tc_fence_after();
+          issue_pv(1, slot, j > 0);
+        }
+        mma_commit(v_empty + slot);
+        if (more) {
+          if (has1) { issue_qk(1, slot1); mma_commit(s_full + 1); }
+          mma_commit(k_empty + slot1);
+        }
       }
       mma_commit(o_full);
     }
@@ -289,15 +284,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const int quad = warp & 3;
       const int r = quad * 32 + lane;  // row of the Q tile == TMEM lane
       const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+      const uint32_t s_tm = tmem + lane_off + tq * 128;
       const uint32_t o_tm = tmem + lane_off + 256 + tq * 128;
       float m = -INFINITY, l = 0.f;
       // invalid columns of tile j (warp-uniform): rows past each kept cluster's end in its last
       // unit, and the padding units after the last kept cluster.  Computed one tile ahead, while
       // the warp waits for the next S, so it is off the softmax critical path.
       int ci = 0;  // cursor over kept clusters: the next one whose last unit is not yet masked
-      uint32_t mw0 = 0, mw1 = 0;
+      uint32_t mw0 = 0, mw1 = 0, mw2 = 0, mw3 = 0;
       auto tile_mask = [&](int j) {
-        mw0 = mw1 = 0;
+        mw0 = mw1 = mw2 = mw3 = 0;
         const int g0 = j * UPT;
         while (ci < nkeep) {
           const int gl = ucum[ci + 1] - 1;  // last unit of kept cluster ci
@@ -306,28 +302,33 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           if (vc < UNIT && gl >= ucum[ci]) {
             const int u = gl - g0;
             const uint32_t bits = ((0xffu << vc) & 0xffu) << (8 * (u & 3));
-            mw0 |= u < 4 ? bits : 0u;
-            mw1 |= u >= 4 ? bits : 0u;
+            const int w = u >> 2;
+            mw0 |= w == 0 ? bits : 0u; mw1 |= w == 1 ? bits : 0u;
+            mw2 |= w == 2 ? bits : 0u; mw3 |= w == 3 ? bits : 0u;
           }
           ++ci;
         }
         if (g0 + UPT > U) {
           for (int u = U - g0; u < UPT; ++u) {
             const uint32_t bits = 0xffu << (8 * (u & 3));
-            mw0 |= u < 4 ? bits : 0u;
-            mw1 |= u >= 4 ? bits : 0u;
+            const int w = u >> 2;
+            mw0 |= w == 0 ? bits : 0u; mw1 |= w == 1 ? bits : 0u;
+            mw2 |= w == 2 ? bits : 0u; mw3 |= w == 3 ? bits : 0u;
           }
         }
       };
+#ifdef CS_ATTN_DEBUG
+      float dbg_s0_keep = 0.f, dbg_s1_keep = 0.f;
+      uint32_t dbg_mw0_keep = 0;
+#endif
       tile_mask(0);
       for (int j = 0; j < nt; ++j) {
-        const uint32_t s_tm = tmem + lane_off + (tq * 2 + (j & 1)) * 64;
-        mbar_wait(s_full + tq * 2 + (j & 1), (j >> 1) & 1);
+        mbar_wait(s_full + tq, j & 1);
         CS_TRACE(5 + 2 * tq, j);
         tc_fence_after();
         uint32_t su[BN];
-        tmem_ld32(s_tm, su);
-        tmem_ld32(s_tm + 32, su + 32);
+#pragma unroll
+        for (int c = 0; c < BN / 32; ++c) tmem_ld32(s_tm + c * 32, su + c * 32);
         tmem_wait_ld();
 #define CS_APPLY_MASK(W, MWV)                                                        \
   if (MWV) {                                                                         \
@@ -335,9 +336,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   }
         CS_APPLY_MASK(0, mw0)
         CS_APPLY_MASK(1, mw1)
+        CS_APPLY_MASK(2, mw2)
+        CS_APPLY_MASK(3, mw3)
 #undef CS_APPLY_MASK
+#ifdef CS_ATTN_DEBUG
+        if (j == 0) { dbg_s0_keep = __uint_as_float(su[0]); dbg_s1_keep = __uint_as_float(su[1]); dbg_mw0_keep = mw0; }
+#endif
         CS_TRACE(16 + tq, j);
-        // row max of the raw scores: 8 independent 3-input max chains over the 64 columns
+        // row max of the raw scores: 8 independent 3-input max chains
         float mx8[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) mx8[i] = fmaxf(__uint_as_float(su[i]), __uint_as_float(su[8 + i]));
@@ -358,12 +364,18 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
         // tcgen05.ld/st are warp-collective (.sync.aligned): rescale if any row of the warp needs it
         const bool warp_rescale = __any_sync(0xffffffffu, alpha != 1.f);
-        // p = 2^(s*scale_log2 - m): paired FFMA2, MUFU ex2 / FMA-pipe polynomial, 4 FADD2 chains
+        // p = 2^(s*scale_log2 - m): paired FFMA2, MUFU ex2, 4 independent FADD2 row-sum chains
         const float2 sl2 = make_float2(scale_log2, scale_log2), nm2 = make_float2(-m, -m);
         float2 acc4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
         for (int c = 0; c < BN; c += 2) {
+#ifdef CS_EXP_OLD
+          const float2 x = make_float2(__uint_as_float(su[c]) * scale_log2 - m, __uint_as_float(su[c + 1]) * scale_log2 - m);
+#else
           const float2 x = ffma2(make_float2(__uint_as_float(su[c]), __uint_as_float(su[c + 1])), sl2, nm2);
+#endif
+          // every 4th pair on the FMA pipe (polynomial), the rest on MUFU: keeps MUFU below the
+          // tensor-core time of the two ping-ponged tiles
           const float2 p = (kPolyEvery > 0 && ((c >> 1) % kPolyEvery) == kPolyEvery - 1)
                                ? ex2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
           acc4[(c >> 1) & 3] = fadd2(acc4[(c >> 1) & 3], p);
@@ -374,10 +386,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         l += s4.x + s4.y;
         CS_TRACE(14 + tq, j);
         tmem_st32(s_tm, su);
-        if (warp_rescale) {
-          // lazy O rescale: PV(j-1) of this tile must have landed in O first
-          mbar_wait(o_ready + tq, (j - 1) & 1);
-          tc_fence_after();
+        tmem_st32(s_tm + 32, su + 32);
+        if (warp_rescale) {  // lazy O rescale; PV(j) is not issued before p_full(j)
 #pragma unroll 1
           for (int c = 0; c < D / 32; ++c) {
             uint32_t ov[32];
@@ -390,7 +400,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
         tmem_wait_st();
         tc_fence_before();
-        mbar_arrive(p_full + tq * 2 + (j & 1));
+        mbar_arrive(p_full + tq);
         CS_TRACE(6 + 2 * tq, j);
         if (j + 1 < nt) tile_mask(j + 1);
       }
@@ -412,6 +422,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
         for (int i = 0; i < 16; ++i)
           pk[i] = pack_bf16x2(__uint_as_float(ov[2 * i]) * inv_l, __uint_as_float(ov[2 * i + 1]) * inv_l);
+#ifdef CS_ATTN_DEBUG
+        if (c == 0) {
+          pk[0] = __float_as_uint(m); pk[1] = __float_as_uint(l); pk[2] = __float_as_uint(dbg_s0_keep);
+          pk[3] = __float_as_uint(dbg_s1_keep); pk[4] = dbg_mw0_keep; pk[5] = (uint32_t)nt; pk[6] = (uint32_t)U;
+          pk[7] = (uint32_t)nkeep;
+        }
+#endif
         if (row_ok) {
           uint4* d4 = reinterpret_cast<uint4*>(dst + c * 32);
 #pragma unroll

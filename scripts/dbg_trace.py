@@ -27,3 +27,12 @@ print('MMA: p_arr0(j) -> PV0 issued', med(buf[4, s] - buf[6, s]), '| QK(j+1) k_f
 print('MMA: v_full seen(j) - p0 seen(j)', med(buf[3, s] - buf[4, s]))
 print('producer: K issue after k_empty', med(buf[0, s] - buf[9, s]), 'V issue after v_empty', med(buf[1, s] - buf[10, s]))
 print('K issued(j) -> k_full seen(j)', med(buf[2, s] - buf[0, s]), 'V issued(j) -> v_full seen(j)', med(buf[3, s] - buf[1, s]))
+j = np.arange(3, nt - 3)
+print('MMA: QK(j+1) issue time [k_full(j+1) seen -> v_full(j) seen]', med(buf[3, j] - buf[2, j + 1]))
+print('MMA: prev PV1(j-1) issued -> k_full(j+1) seen', med(buf[2, j + 1] - buf[11, j - 1]))
+print('MMA: v_full(j) seen -> p0(j) seen', med(buf[4, j] - buf[3, j]), ' p0 -> p1 seen', med(buf[11, j] - buf[4, j]))
+print('producer K: issued(j+1) vs MMA k_full(j+1) seen', med(buf[2, j + 1] - buf[0, j + 1]))
+print('raw j=10..13 events (rel):')
+for jj in range(10, 14):
+    t0 = buf[5, jj]
+    print(jj, {n: int(buf[e, jj] - t0) for n, e in [('Kiss', 0), ('Viss', 1), ('kf', 2), ('vf', 3), ('p0', 4), ('p1', 11), ('S0', 5), ('P0', 6), ('S1', 7), ('P1', 8)]})
