@@ -107,9 +107,9 @@ def _cuda(t: torch.Tensor, name: str):
 
 def launches_per_layer(iters: int) -> int:
     """Kernels the fused entry launches per layer: init_sample 1; per iteration and side: anchor
-    prep 2 + assign GEMM 1 + counting sort 3 + centroid update 1; selection 3; V permute 1;
-    work list 1; attention 1."""
-    return 1 + iters * 2 * 7 + 3 + 1 + 1 + 1
+    prep 2 + assign GEMM 1 + counting sort 3 + centroid update 1; selection 4 (Abar, rows,
+    count, emit); V permute 1; work list 1; attention 1."""
+    return 1 + iters * 2 * 7 + 4 + 1 + 1 + 1
 
 
 def workspace_bytes(B, H, N, d, kq, kk) -> int:
@@ -198,7 +198,7 @@ def block_select(cq, ck, offs_q, offs_k, budget, tau=0.95, theta=0.1, rule=RULE_
     kk = ck.shape[2]
     n_keep = torch.empty(B, H, dtype=torch.int32, device=cq.device)
     kept = torch.full((B, H, kq, kk), -1, dtype=torch.int32, device=cq.device)
-    w, wn = _ws(ws, B * H * kq * (kk + 1) * 4 + 4096, cq.device)
+    w, wn = _ws(ws, B * H * kq * (kk + 1) * 4 + B * H * kq * kk * 8 + 4096, cq.device)
     _check(lib().block_select(B, H, kq, kk, d, _ptr(cq.contiguous()), _ptr(ck.contiguous()),
                               _ptr(offs_q), _ptr(offs_k), _ptr(budget), float(tau), float(theta),
                               int(rule), _ptr(n_keep), _ptr(kept), w, wn, _stream(cq)))

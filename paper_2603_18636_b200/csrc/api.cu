@@ -75,11 +75,13 @@ AssignScratch carve_assign(Carve& c, int BH, int N, int d, int kq, int kk) {
 struct SelectScratch {
   int32_t* order;
   int32_t* cnt;
+  double* abar;
 };
 SelectScratch carve_select(Carve& c, int BH, int kq, int kk) {
   SelectScratch s;
   s.order = c.take<int32_t>((size_t)BH * kq * kk);
   s.cnt = c.take<int32_t>((size_t)BH * kq);
+  s.abar = c.take<double>((size_t)BH * kq * kk);
   return s;
 }
 struct AttnScratch {
@@ -394,7 +396,7 @@ cs_status block_select(int B, int H, int kq, int kk, int d, const float* cq, con
   Carve c(ws);
   SelectScratch sc = carve_select(c, BH, kq, kk);
   CS_CUDA(launch_block_select(BH, H, kq, kk, d, cq, ck, offs_q, offs_k, budget, tau, theta, rule, n_keep, kept,
-                              sc.order, sc.cnt, static_cast<cudaStream_t>(stream)),
+                              sc.order, sc.cnt, sc.abar, static_cast<cudaStream_t>(stream)),
           "block_select");
   return CS_OK;
 }
@@ -457,7 +459,7 @@ cs_status coclust_sparse_attention(int B, int H, int N, int d, cs_bf16_in q, cs_
                       s.offs_q, s.perm_k, s.offs_k, as, at.qp, at.kp, st));
   if (stage_events) CS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(stage_events[0]), st), "event");
   CS_CUDA(launch_block_select(BH, H, kq, kk, d, s.cq, s.ck, s.offs_q, s.offs_k, budget, tau, theta, rule,
-                              s.n_keep, s.kept, se.order, se.cnt, st),
+                              s.n_keep, s.kept, se.order, se.cnt, se.abar, st),
           "block_select");
   if (stage_events) CS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(stage_events[1]), st), "event");
   CS_CUDA(launch_permute_rows(view(v, H), BH, N, d, s.perm_k, at.vp, st), "permute_v");

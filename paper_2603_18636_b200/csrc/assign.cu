@@ -56,6 +56,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
   const int warp = warp_id(), lane = lane_id();
   const int nchunks = ks_pad / nch;
+  // contiguous unit range per CTA: consecutive units mostly share the head, so when the whole
+  // centroid side fits the W ring (one chunk) it stays resident in SMEM across units
+  const int upc = (num_units + gridDim.x - 1) / gridDim.x;
+  const int u_begin = blockIdx.x * upc, u_end = min(num_units, u_begin + upc);
   constexpr int SLABS = 2 * D / 64;  // 64-column slabs per chunk (hi halves then lo halves)
 
   if (threadIdx.x == 0) {
@@ -75,8 +79,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       tma_prefetch_desc(&tm_x);
       tma_prefetch_desc(&tm_w);
       int g = 0;  // global slab counter
-      int it = 0;
-      for (int u = blockIdx.x; u < num_units; u += gridDim.x, ++it) {
+      int it = 0, prev_bh = -1;
+      for (int u = u_begin; u < u_end; ++u, ++it) {
         const int bh = u / units_per_head, n0 = (u % units_per_head) * (TILES * BM);
         const int b = bh / H, h = bh % H;
         const int xs = it & 1;
@@ -86,14 +90,20 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           for (int hf = 0; hf < L::HALVES; ++hf)
             tma_load_4d(sm + L::OFF_X + xs * L::XSTAGE + t * L::XT + hf * L::HALF_X, &tm_x, hf * 64,
                         n0 + t * BM, h, b, x_full + xs);
+        const bool w_resident = nchunks == 1 && SLABS == NSTW && bh == prev_bh;
         for (int c = 0; c < nchunks; ++c)
           for (int s = 0; s < SLABS; ++s, ++g) {
             const int stage = g % NSTW;
             mbar_wait(w_empty + stage, ((g / NSTW) & 1) ^ 1);
-            mbar_arrive_expect_tx(w_full + stage, nch * 128);
-            tma_load_2d(sm + L::OFF_W + stage * L::SLAB, &tm_w, s * 64, bh * ks_pad + c * nch,
-                        w_full + stage);
+            if (w_resident) {
+              mbar_arrive(w_full + stage);  // same head, same slab already in this stage
+            } else {
+              mbar_arrive_expect_tx(w_full + stage, nch * 128);
+              tma_load_2d(sm + L::OFF_W + stage * L::SLAB, &tm_w, s * 64, bh * ks_pad + c * nch,
+                          w_full + stage);
+            }
           }
+        prev_bh = bh;
       }
     }
   } else if (warp == WARP_MMA) {
@@ -101,7 +111,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const uint32_t idesc = idesc_bf16(BM, nch, 0, 0);
       const uint32_t sX = smem_u32(sm + L::OFF_X), sW = smem_u32(sm + L::OFF_W);
       int g = 0, gc = 0, it = 0;
-      for (int u = blockIdx.x; u < num_units; u += gridDim.x, ++it) {
+      for (int u = u_begin; u < u_end; ++u, ++it) {
         const int xs = it & 1;
         mbar_wait(x_full + xs, (it >> 1) & 1);
         for (int c = 0; c < nchunks; ++c, ++gc) {
@@ -137,7 +147,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const int r = quad * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
     int gc = 0;
-    for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+    for (int u = u_begin; u < u_end; ++u) {
       const int bh = u / units_per_head, n0 = (u % units_per_head) * (TILES * BM);
       float best = -INFINITY;
       int best_j = 0;

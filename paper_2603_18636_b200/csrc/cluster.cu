@@ -72,7 +72,10 @@ __global__ void __launch_bounds__(256) k_init_sample(XView q, XView k, int N, in
         z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
         z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
         z ^= z >> 31;
-        const int t = (int)(z % (unsigned long long)(j + 1));
+        // z mod m = ((z_hi mod m) * 2^32 + z_lo) mod m, the second step on a value < m * 2^32
+        const unsigned m = (unsigned)(j + 1);
+        const unsigned long long hi_r = (unsigned long long)((unsigned)(z >> 32) % m);
+        const int t = (int)(((hi_r << 32) | (z & 0xffffffffull)) % m);
         const int pick = ((sm_bits[t >> 5] >> (t & 31)) & 1u) ? j : t;
         sm_bits[pick >> 5] |= 1u << (pick & 31);
       }
@@ -94,23 +97,31 @@ __global__ void __launch_bounds__(256) k_init_sample(XView q, XView k, int N, in
     }
   }
   __syncthreads();
-  // C^(0)[j] = X[idx[j]]  (bf16 -> fp32)
+  // C^(0)[j] = X[idx[j]]  (bf16 -> fp32): 8 bf16 (16 B) per thread and load
   const int b = bh / X.H, h = bh % X.H;
-  for (int e = threadIdx.x; e < K * d; e += blockDim.x) {
-    const int j = e / d, c = e % d;
-    C[e] = __bfloat162float(X.row(b, h, idx[j])[c]);
+  const int vpr = d / 8;  // 16-byte vectors per row
+  for (int e = threadIdx.x; e < K * vpr; e += blockDim.x) {
+    const int j = e / vpr, c = (e % vpr) * 8;
+    const uint4 v = *reinterpret_cast<const uint4*>(X.row(b, h, idx[j]) + c);
+    const __nv_bfloat16* pv = reinterpret_cast<const __nv_bfloat16*>(&v);
+    float4 lo, hi;
+    lo.x = __bfloat162float(pv[0]); lo.y = __bfloat162float(pv[1]); lo.z = __bfloat162float(pv[2]); lo.w = __bfloat162float(pv[3]);
+    hi.x = __bfloat162float(pv[4]); hi.y = __bfloat162float(pv[5]); hi.z = __bfloat162float(pv[6]); hi.w = __bfloat162float(pv[7]);
+    float4* dst = reinterpret_cast<float4*>(C + (size_t)j * d + c);
+    dst[0] = lo;
+    dst[1] = hi;
   }
 }
 
 // ---------------------------------------------------------------------------------------------
-// a2: Gamma = C_a^T C_a (fp64).  grid (BH, d/16), block 256: rows e in [16 by, 16 by + 16).
+// a2: Gamma = C_a^T C_a (fp64).  grid (BH, d/8), block 256: rows e in [8 by, 8 by + 8).
 // Thread t owns column f = t % d and rows e0 + t/d + EB*i: the staged row r is read along f
 // (conflict-free) and at e (warp-uniform broadcast).
 // ---------------------------------------------------------------------------------------------
 template <int D>
 __global__ void __launch_bounds__(256) k_gamma(const float* __restrict__ ca, int ka,
                                                double* __restrict__ gamma) {
-  constexpr int ROWS = 16, CH = 32, EB = 256 / D, RPT = ROWS / EB;
+  constexpr int ROWS = 8, CH = 32, EB = 256 / D, RPT = ROWS / EB;
   __shared__ double sa[CH][D];
   const int bh = blockIdx.x, e0 = blockIdx.y * ROWS;
   const float* A = ca + (size_t)bh * ka * D;
@@ -162,6 +173,7 @@ __global__ void __launch_bounds__(256, 1) k_anchor_w(const float* __restrict__ c
   double w[RPT];
 #pragma unroll
   for (int i = 0; i < RPT; ++i) w[i] = 0.0;
+#pragma unroll 16
   for (int f = 0; f < D; ++f) {
     const double g = G[(size_t)f * D + e];
 #pragma unroll
@@ -207,47 +219,49 @@ __global__ void __launch_bounds__(256) k_seg_mean(XView x, int N, int K,
                                                   const int32_t* __restrict__ offs,
                                                   float* __restrict__ C,
                                                   __nv_bfloat16* __restrict__ xperm) {
-  constexpr int VEC = D / 32;  // bf16 per lane (4 or 2)
-  constexpr int NW = 8, U = 8;
-  __shared__ float part[NW][D];
+  constexpr int LPR = D / 8;        // lanes per row: 16-byte (8 x bf16) vector per lane
+  constexpr int RPW = 32 / LPR;     // rows per warp instruction (2 or 4)
+  constexpr int NW = 8, U = 8;      // warps, rows in flight per lane group
+  __shared__ float part[NW * RPW][D];
   const int bh = blockIdx.y, j = blockIdx.x;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int grp = lane / LPR, gl = lane % LPR;  // row group inside the warp, lane inside the row
   const int32_t* of = offs + (size_t)bh * (K + 1);
   const int beg = of[j], end = of[j + 1], cnt = end - beg;
   if (cnt == 0) return;
   const int b = bh / x.H, h = bh % x.H;
+  // fixed partition of the cluster's positions: warp w owns a contiguous chunk, row group grp
+  // takes every RPW-th position of it -> deterministic summation order
   const int chunk = (cnt + NW - 1) / NW;
   const int p0 = beg + w * chunk, p1 = min(end, p0 + chunk);
   const int32_t* pm = perm + (size_t)bh * N;
-  float acc[VEC];
+  float acc[8];
 #pragma unroll
-  for (int i = 0; i < VEC; ++i) acc[i] = 0.f;
-  using VT = typename std::conditional<VEC == 4, uint2, uint32_t>::type;
-  for (int p = p0; p < p1; p += U) {
-    VT v[U];
+  for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+  for (int p = p0 + grp; p < p1; p += U * RPW) {
+    uint4 v[U];
     int tok[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) tok[u] = (p + u < p1) ? pm[p + u] : -1;
+    for (int u = 0; u < U; ++u) tok[u] = (p + u * RPW < p1) ? pm[p + u * RPW] : -1;
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      if (tok[u] >= 0) v[u] = *reinterpret_cast<const VT*>(x.row(b, h, tok[u]) + lane * VEC);
+      if (tok[u] >= 0) v[u] = *reinterpret_cast<const uint4*>(x.row(b, h, tok[u]) + gl * 8);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       if (tok[u] < 0) break;
       const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&v[u]);
 #pragma unroll
-      for (int i = 0; i < VEC; ++i) acc[i] += __bfloat162float(e[i]);
-      if (xperm)
-        *reinterpret_cast<VT*>(xperm + ((size_t)bh * N + p + u) * D + lane * VEC) = v[u];
+      for (int i = 0; i < 8; ++i) acc[i] += __bfloat162float(e[i]);
+      if (xperm) *reinterpret_cast<uint4*>(xperm + ((size_t)bh * N + p + u * RPW) * D + gl * 8) = v[u];
     }
   }
 #pragma unroll
-  for (int i = 0; i < VEC; ++i) part[w][lane * VEC + i] = acc[i];
+  for (int i = 0; i < 8; ++i) part[w * RPW + grp][gl * 8 + i] = acc[i];
   __syncthreads();
   if (threadIdx.x < D) {
     float s = 0.f;
 #pragma unroll
-    for (int ww = 0; ww < NW; ++ww) s += part[ww][threadIdx.x];
+    for (int q = 0; q < NW * RPW; ++q) s += part[q][threadIdx.x];
     C[((size_t)bh * K + j) * D + threadIdx.x] = s / (float)cnt;
   }
 }
@@ -362,10 +376,10 @@ cudaError_t launch_init_sample(XView q, XView k, int BH, int N, int d, int kq, i
 cudaError_t launch_anchor_prep(const float* ca, int ka, const float* cself, int ks, int ks_pad,
                                int BH, int d, double* gamma, __nv_bfloat16* wsplit, cudaStream_t st) {
   if (d == 128) {
-    k_gamma<128><<<dim3(BH, 128 / 16), 256, 0, st>>>(ca, ka, gamma);
+    k_gamma<128><<<dim3(BH, 128 / 8), 256, 0, st>>>(ca, ka, gamma);
     k_anchor_w<128><<<dim3((ks_pad + 31) / 32, BH), 256, 0, st>>>(cself, ks, ks_pad, gamma, wsplit);
   } else {
-    k_gamma<64><<<dim3(BH, 64 / 16), 256, 0, st>>>(ca, ka, gamma);
+    k_gamma<64><<<dim3(BH, 64 / 8), 256, 0, st>>>(ca, ka, gamma);
     k_anchor_w<64><<<dim3((ks_pad + 31) / 32, BH), 256, 0, st>>>(cself, ks, ks_pad, gamma, wsplit);
   }
   return cudaGetLastError();

@@ -49,7 +49,7 @@ cudaError_t launch_block_select(int BH, int H, int kq, int kk, int d, const floa
                                 const float* ck, const int32_t* offs_q, const int32_t* offs_k,
                                 const float* budget, double tau, double theta, int rule,
                                 int32_t* n_keep, int32_t* kept, int32_t* order, int32_t* cnt,
-                                cudaStream_t st);
+                                double* abar, cudaStream_t st);
 cudaError_t launch_worklist(int BH, int kq, const int32_t* offs_q, int32_t* item_start,
                             cudaStream_t st);
 int worklist_upper_bound(int N, int kq);

@@ -15,9 +15,41 @@ __device__ __forceinline__ bool before(double va, int ia, double vb, int ib) {
   return va > vb || (va == vb && ia < ib);
 }
 
+// Abar = C_q C_k^T in fp64.  grid (ceil(kk/32), ceil(kq/16), BH), block 256: a 16 x 32
+// output tile, each thread two dot products of length D in a fixed (sequential) order.
+template <int D>
+__global__ void __launch_bounds__(256) k_abar(int kq, int kk, const float* __restrict__ cq,
+                                              const float* __restrict__ ck, double* __restrict__ abar) {
+  __shared__ double sq[16][D];
+  __shared__ float sk[32][D + 1];
+  const int bh = blockIdx.z, a0 = blockIdx.y * 16, j0 = blockIdx.x * 32, t = threadIdx.x;
+  for (int i = t; i < 16 * D; i += 256) {
+    const int r = i / D, c = i % D;
+    sq[r][c] = (a0 + r < kq) ? (double)cq[((size_t)bh * kq + a0 + r) * D + c] : 0.0;
+  }
+  for (int i = t; i < 32 * D; i += 256) {
+    const int r = i / D, c = i % D;
+    sk[r][c] = (j0 + r < kk) ? ck[((size_t)bh * kk + j0 + r) * D + c] : 0.f;
+  }
+  __syncthreads();
+  const int al = t >> 4, jl = t & 15;
+  double s0 = 0.0, s1 = 0.0;
+#pragma unroll 8
+  for (int e = 0; e < D; ++e) {
+    const double q = sq[al][e];
+    s0 = fma(q, (double)sk[jl][e], s0);
+    s1 = fma(q, (double)sk[jl + 16][e], s1);
+  }
+  const int a = a0 + al;
+  if (a < kq) {
+    double* row = abar + ((size_t)bh * kq + a) * kk;
+    if (j0 + jl < kk) row[j0 + jl] = s0;
+    if (j0 + jl + 16 < kk) row[j0 + jl + 16] = s1;
+  }
+}
+
 // grid (kq, BH), block 256, dyn smem: P2 doubles + P2 ints + d doubles
-__global__ void __launch_bounds__(256) k_select_rows(int kq, int kk, int d, const float* __restrict__ cq,
-                                                     const float* __restrict__ ck,
+__global__ void __launch_bounds__(256) k_select_rows(int kq, int kk, int d, const double* __restrict__ abar,
                                                      const int32_t* __restrict__ offs_q,
                                                      const int32_t* __restrict__ offs_k, double tau,
                                                      int32_t* __restrict__ order, int32_t* __restrict__ cnt) {
@@ -32,23 +64,11 @@ __global__ void __launch_bounds__(256) k_select_rows(int kq, int kk, int d, cons
   const int a = blockIdx.x, bh = blockIdx.y, t = threadIdx.x;
   const int32_t* ok = offs_k + (size_t)bh * (kk + 1);
   const int32_t* oq = offs_q + (size_t)bh * (kq + 1);
-  const float* crow = cq + ((size_t)bh * kq + a) * d;
   (void)scq;
-  // Abar_a = C_q[a] . C_k[j] in fp64: one warp per key centroid, lanes along d (coalesced)
-  const int lane = t & 31, wp = t >> 5;
-  const int vpl = d / 32;  // 4 (d=128) or 2 (d=64)
-  double cqv[4];
-  for (int i = 0; i < vpl; ++i) cqv[i] = (double)crow[lane * vpl + i];
-  for (int j = wp; j < P2; j += 8) {
-    double v = -INFINITY;
-    if (j < kk && ok[j + 1] - ok[j] > 0) {
-      const float* kr = ck + ((size_t)bh * kk + j) * d + lane * vpl;
-      double acc = 0.0;
-      for (int i = 0; i < vpl; ++i) acc = fma(cqv[i], (double)kr[i], acc);
-      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      v = acc;
-    }
-    if (lane == 0) { sval[j] = v; sidx[j] = j; }
+  const double* arow = abar + ((size_t)bh * kq + a) * kk;
+  for (int j = t; j < P2; j += 256) {
+    sval[j] = (j < kk && ok[j + 1] - ok[j] > 0) ? arow[j] : -INFINITY;
+    sidx[j] = j;
   }
   __syncthreads();
   // bitonic sort: (value desc, index asc)
@@ -235,11 +255,15 @@ cudaError_t launch_block_select(int BH, int H, int kq, int kk, int d, const floa
                                 const float* ck, const int32_t* offs_q, const int32_t* offs_k,
                                 const float* budget, double tau, double theta, int rule,
                                 int32_t* n_keep, int32_t* kept, int32_t* order, int32_t* cnt,
-                                cudaStream_t st) {
+                                double* abar, cudaStream_t st) {
   int P2 = 1;
   while (P2 < kk) P2 <<= 1;
   const size_t smem = (size_t)P2 * 8 + (size_t)d * 8 + (size_t)P2 * 4;
-  k_select_rows<<<dim3(kq, BH), 256, smem, st>>>(kq, kk, d, cq, ck, offs_q, offs_k, tau, order, cnt);
+  if (d == 128)
+    k_abar<128><<<dim3((kk + 31) / 32, (kq + 15) / 16, BH), 256, 0, st>>>(kq, kk, cq, ck, abar);
+  else
+    k_abar<64><<<dim3((kk + 31) / 32, (kq + 15) / 16, BH), 256, 0, st>>>(kq, kk, cq, ck, abar);
+  k_select_rows<<<dim3(kq, BH), 256, smem, st>>>(kq, kk, d, abar, offs_q, offs_k, tau, order, cnt);
   k_select_count<<<BH, 1024, 0, st>>>(H, kq, kk, offs_q, offs_k, cnt, budget, theta, rule, n_keep);
   k_select_emit<<<dim3(kq, BH), 256, 0, st>>>(kq, kk, order, n_keep, kept);
   return cudaGetLastError();
