@@ -213,70 +213,79 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       if (lane == 0) CS_TRACE(is_v ? 1 : 0, jj);
     }
   } else if (warp == WARP_MMA) {
-    // ================= MMA issuer (one thread) =================
-    if (lane == 0) {
-      constexpr uint32_t idesc_qk = idesc_bf16(BM, BN, 0, 0);
-      constexpr uint32_t idesc_pv = idesc_bf16(BM, D, 0, 1);
-      const uint32_t sQ = smem_u32(sm + L::OFF_Q), sK = smem_u32(sm + L::OFF_K),
-                     sV = smem_u32(sm + L::OFF_V);
-      auto issue_qk = [&](int tq, int slot) {
+    // ================= MMA issuer (whole warp, one elected lane issues) =================
+    // Descriptors are built once; inside the loop a K-step or a ring slot is a constant offset
+    // added to the 14-bit start-address field (addresses stay < 256 KB, so no carry out).
+    constexpr uint32_t idesc_qk = idesc_bf16(BM, BN, 0, 0);
+    constexpr uint32_t idesc_pv = idesc_bf16(BM, D, 0, 1);
+    const uint64_t dq0 = smem_desc_sw128(smem_u32(sm + L::OFF_Q), 16, 1024);
+    const uint64_t dk0 = smem_desc_sw128(smem_u32(sm + L::OFF_K), 16, 1024);
+    const uint64_t dv0 = smem_desc_sw128(smem_u32(sm + L::OFF_V), L::HALF_K, 1024);
+    auto issue_qk = [&](int tq, int slot) {
+      if (elect_one()) {
         const uint32_t d_tmem = tmem + tq * 128;
+        const uint64_t qd = dq0 + (uint64_t)((tq * L::QT) >> 4);
+        const uint64_t kd = dk0 + (uint64_t)((slot * L::KT) >> 4);
 #pragma unroll
         for (int kk2 = 0; kk2 < D / 16; ++kk2) {
-          const uint32_t off = (kk2 >> 2) * L::HALF_Q + (kk2 & 3) * 32;
-          const uint32_t offk = (kk2 >> 2) * L::HALF_K + (kk2 & 3) * 32;
-          const uint64_t ad = smem_desc_sw128(sQ + tq * L::QT + off, 16, 1024);
-          const uint64_t bd = smem_desc_sw128(sK + slot * L::KT + offk, 16, 1024);
-          mma_ss(d_tmem, ad, bd, idesc_qk, kk2 > 0);
-        }
-      };
-      auto issue_pv = [&](int tq, int slot, bool acc) {
-        const uint32_t d_tmem = tmem + 256 + tq * 128;
-        const uint32_t p_tmem = tmem + tq * 128;
-#pragma unroll
-        for (int kk2 = 0; kk2 < BN / 16; ++kk2) {
-          const uint64_t bd = smem_desc_sw128(sV + slot * L::KT + kk2 * 2048, L::HALF_K, 1024);
-          mma_ts(d_tmem, p_tmem + kk2 * 8, bd, idesc_pv, (acc || kk2 > 0) ? 1u : 0u);
-        }
-      };
-      mbar_wait(q_full, 0);
-      mbar_wait(k_full, 0);
-      tc_fence_after();
-      issue_qk(0, 0);
-      mma_commit(s_full + 0);
-      if (has1) { issue_qk(1, 0); mma_commit(s_full + 1); }
-      mma_commit(k_empty + 0);
-      for (int j = 0; j < nt; ++j) {
-        const int slot = j % NST, slot1 = (j + 1) % NST;
-        const bool more = j + 1 < nt;
-        mbar_wait(p_full + 0, j & 1);
-        CS_TRACE(4, j);
-        mbar_wait(v_full + slot, (j / NST) & 1);
-        CS_TRACE(3, j);
-        tc_fence_after();
-        issue_pv(0, slot, j > 0);
-        if (more) {
-          mbar_wait(k_full + slot1, ((j + 1) / NST) & 1);
-          CS_TRACE(2, j + 1);
-          tc_fence_after();
-          issue_qk(0, slot1);
-          mma_commit(s_full + 0);
-        }
-        if (has1) {
-          mbar_wait(p_full + 1, j & 1);
-          CS_TRACE(11, j);
-          tc_fence_after();
-          issue_pv(1, slot, j > 0);
-        }
-        mma_commit(v_empty + slot);
-        if (more) {
-          if (has1) { issue_qk(1, slot1); mma_commit(s_full + 1); }
-          mma_commit(k_empty + slot1);
+          const uint32_t off = ((kk2 >> 2) * L::HALF_Q + (kk2 & 3) * 32) >> 4;
+          const uint32_t offk = ((kk2 >> 2) * L::HALF_K + (kk2 & 3) * 32) >> 4;
+          mma_ss(d_tmem, qd + off, kd + offk, idesc_qk, kk2 > 0);
         }
       }
-      mma_commit(o_full);
+      __syncwarp();
+    };
+    auto issue_pv = [&](int tq, int slot, bool acc) {
+      if (elect_one()) {
+        const uint32_t d_tmem = tmem + 256 + tq * 128;
+        const uint32_t p_tmem = tmem + tq * 128;
+        const uint64_t vd = dv0 + (uint64_t)((slot * L::KT) >> 4);
+#pragma unroll
+        for (int kk2 = 0; kk2 < BN / 16; ++kk2)
+          mma_ts(d_tmem, p_tmem + kk2 * 8, vd + (uint64_t)((kk2 * 2048) >> 4), idesc_pv, (acc || kk2 > 0) ? 1u : 0u);
+      }
+      __syncwarp();
+    };
+    auto commit = [&](uint64_t* bar) {
+      if (elect_one()) mma_commit(bar);
+      __syncwarp();
+    };
+    mbar_wait(q_full, 0);
+    mbar_wait(k_full, 0);
+    tc_fence_after();
+    issue_qk(0, 0);
+    commit(s_full + 0);
+    if (has1) { issue_qk(1, 0); commit(s_full + 1); }
+    commit(k_empty + 0);
+    for (int j = 0; j < nt; ++j) {
+      const int slot = j % NST, slot1 = (j + 1) % NST;
+      const bool more = j + 1 < nt;
+      mbar_wait(p_full + 0, j & 1);
+      CS_TRACE(4, j);
+      mbar_wait(v_full + slot, (j / NST) & 1);
+      CS_TRACE(3, j);
+      tc_fence_after();
+      issue_pv(0, slot, j > 0);
+      if (more) {
+        mbar_wait(k_full + slot1, ((j + 1) / NST) & 1);
+        CS_TRACE(2, j + 1);
+        tc_fence_after();
+        issue_qk(0, slot1);
+        commit(s_full + 0);
+      }
+      if (has1) {
+        mbar_wait(p_full + 1, j & 1);
+        CS_TRACE(11, j);
+        tc_fence_after();
+        issue_pv(1, slot, j > 0);
+      }
+      commit(v_empty + slot);
+      if (more) {
+        if (has1) { issue_qk(1, slot1); commit(s_full + 1); }
+        commit(k_empty + slot1);
+      }
     }
-    __syncwarp();
+    commit(o_full);
   } else {
     // ================= softmax / epilogue (warps 0-7) =================
     const int tq = warp >> 2;

@@ -16,6 +16,17 @@ CS_DEV uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 CS_DEV int lane_id() { return threadIdx.x & 31; }
+// true in exactly one (the same) lane of the converged warp
+CS_DEV bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .b32 %%rx;\n\t.reg .pred %%px;\n\t"
+      "elect.sync %%rx|%%px, %1;\n\t"
+      "@%%px mov.s32 %0, 1;\n\t}"
+      : "+r"(pred)
+      : "r"(0xffffffffu));
+  return pred != 0;
+}
 CS_DEV int warp_id() { return __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0); }
 
 // ------------------------------------------------------------------ mbarrier
