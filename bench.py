@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--parallel", choices=["head", "ulysses"], default=None,
+                    help="multi-GPU split (default: ulysses for hunyuan_720p, head-parallel otherwise)")
     ap.add_argument("--cpu-sample-rows", type=int, default=1500,
                     help="query rows of the oracle attention sample")
     return ap.parse_args()
@@ -185,31 +187,51 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     c = CONFIGS[args.config]
     H_total, d = c["H"], c["d"]
-    h0, h1 = head_range(H_total, world, rank)
-    # deterministic per-head generation: every rank builds exactly its heads of the full layer
-    full = video_qkv(c["T"], c["Hs"], c["Ws"], H_total, d, seed=args.seed, device=dev) if world == 1 else None
-    if full is None:
-        parts = [video_qkv(c["T"], c["Hs"], c["Ws"], H_total, d, seed=args.seed, device=dev)]
-        q, k, v = (t[:, h0:h1].contiguous() for t in (parts[0].q, parts[0].k, parts[0].v))
-        del parts
-    else:
-        q, k, v = full.q, full.k, full.v
-    B, H, N, _ = q.shape
-    budget = torch.full((H,), args.budget, dtype=torch.float32, device=dev)
+    mode = args.parallel or ("ulysses" if (args.config == "hunyuan_720p" and world > 1) else "head")
+    # deterministic generation: every rank builds the full layer and keeps its share
+    full = video_qkv(c["T"], c["Hs"], c["Ws"], H_total, d, seed=args.seed, device=dev)
+    N = full.q.shape[2]
     rule = RULES[args.rule]
     ws = pb.Workspace()
-    out = torch.empty_like(q)
-    kw = dict(seed=args.seed, tau=args.tau, theta=args.theta, rule=rule, out=out, ws=ws, head_offset=h0,
-              heads_total=H_total)
+    budget_all = torch.full((H_total,), args.budget, dtype=torch.float32, device=dev)
+    if mode == "ulysses":
+        from paper_2603_18636_b200.dist import ulysses_layer
+        if H_total % world or N % world:
+            raise SystemExit("Ulysses needs H and N divisible by the number of GPUs")
+        Hl, Nl = H_total // world, N // world
+        h0, h1 = rank * Hl, (rank + 1) * Hl
+        tok = lambda t: t[0].permute(1, 0, 2)[rank * Nl:(rank + 1) * Nl].unsqueeze(0).contiguous()
+        q, k, v = tok(full.q), tok(full.k), tok(full.v)          # [1, N/P, H, d] token blocks
+        q_h, k_h = full.q[:, h0:h1].contiguous(), full.k[:, h0:h1].contiguous()  # for F_kept only
+        kw = dict(seed=args.seed, tau=args.tau, theta=args.theta, rule=rule, ws=ws)
 
-    def step(evs=None):
-        pb.coclust_sparse_attention(q, k, v, args.kq, args.kk, args.iters, budget, stage_events=evs, **kw)
+        def step(evs=None, qq=None, kk_=None, vv=None):
+            return ulysses_layer(q if qq is None else qq, k if kk_ is None else kk_, v if vv is None else vv,
+                                 args.kq, args.kk, args.iters, budget_all, stage_events=evs, **kw)
+    else:
+        h0, h1 = head_range(H_total, world, rank)
+        q, k, v = (t[:, h0:h1].contiguous() for t in (full.q, full.k, full.v))
+        q_h, k_h = q, k
+        out = torch.empty_like(q)
+        budget = budget_all[h0:h1].contiguous()
+        kw = dict(seed=args.seed, tau=args.tau, theta=args.theta, rule=rule, out=out, ws=ws, head_offset=h0,
+                  heads_total=H_total)
 
-    # kept FLOPs of this layer (state recomputed through the staged entries: same kernels, same bits)
-    st = pb.coclust_assign(q, k, args.kq, args.kk, args.iters, seed=args.seed, ws=ws, head_offset=h0,
+        def step(evs=None, qq=None, kk_=None, vv=None):
+            return pb.coclust_sparse_attention(q if qq is None else qq, k if kk_ is None else kk_,
+                                               v if vv is None else vv, args.kq, args.kk, args.iters, budget,
+                                               stage_events=evs, **kw)
+    B = 1
+    H = h1 - h0
+    cpu_src = full if (world == 1 and not args.no_cpu_baseline) else None
+    del full
+
+    # kept FLOPs of this rank's heads (state recomputed through the staged entries: same kernels,
+    # same bits as inside the fused call)
+    st = pb.coclust_assign(q_h, k_h, args.kq, args.kk, args.iters, seed=args.seed, ws=ws, head_offset=h0,
                            heads_total=H_total)
-    n_keep, kept = pb.block_select(st["cq"], st["ck"], st["offs_q"], st["offs_k"], budget, args.tau,
-                                   args.theta, rule, ws=ws)
+    n_keep, kept = pb.block_select(st["cq"], st["ck"], st["offs_q"], st["offs_k"],
+                                   budget_all[h0:h1].contiguous(), args.tau, args.theta, rule, ws=ws)
     torch.cuda.synchronize()
     oq = st["offs_q"].cpu().numpy().reshape(B * H, -1)
     ok = st["offs_k"].cpu().numpy().reshape(B * H, -1)
@@ -220,7 +242,7 @@ def run_ours(args):
         sq, sk = np.diff(oq[bh]), np.diff(ok[bh])
         f_kept += int((sq * sk[kp[bh, :, :nk[bh]]].sum(1)).sum())
     f_kept *= 4 * d
-    del st, n_keep, kept
+    del st, n_keep, kept, q_h, k_h
 
     for _ in range(max(args.warmup, 1)):
         step()
@@ -266,12 +288,13 @@ def run_ours(args):
     e2e = None
     if not args.no_e2e:
         hq, hk, hv = (t.cpu().pin_memory() for t in (q, k, v))
-        ho = torch.empty(out.shape, dtype=out.dtype).pin_memory()
+        o_shape = q.shape
+        ho = torch.empty(o_shape, dtype=q.dtype).pin_memory()
         dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
         def e2e_step():
             dq.copy_(hq, non_blocking=True); dk.copy_(hk, non_blocking=True); dv.copy_(hv, non_blocking=True)
-            pb.coclust_sparse_attention(dq, dk, dv, args.kq, args.kk, args.iters, budget, **kw)
-            ho.copy_(out, non_blocking=True)
+            o = step(qq=dq, kk_=dk, vv=dv)
+            ho.copy_(o, non_blocking=True)
         e2e_step()
         torch.cuda.synchronize()
         if world > 1:
@@ -312,7 +335,7 @@ def run_ours(args):
     dense_flops = 4.0 * B * H_total * N * N * d
     cpu = None
     if not args.no_cpu_baseline and world == 1:
-        v_ms, det = cpu_oracle_sample(full, 0, args.kq, args.kk, args.iters, args.budget, rule, args.tau,
+        v_ms, det = cpu_oracle_sample(cpu_src, 0, args.kq, args.kk, args.iters, args.budget, rule, args.tau,
                                       args.theta, args.seed, H_total, args.cpu_sample_rows)
         cpu = {"value": v_ms, "unit": "ms", "cores": len(os.sched_getaffinity(0)), "kind": "oracle",
                "sample": (f"head 0 of {H_total}: full float64 co-clustering ({args.iters} it, {args.kq}/"
@@ -327,8 +350,8 @@ def run_ours(args):
         "config": {"workload": CONFIG_NAMES[args.config], "B": B, "H": H_total, "N": N, "d": d,
                    "kq": args.kq, "kk": args.kk, "iters": args.iters, "budget": args.budget,
                    "rule": args.rule, "tau": args.tau, "theta": args.theta,
-                   "parallelism": f"head-parallel x{world}", "l2": "inputs larger than L2 (%.0f MB/tensor)"
-                   % (q.numel() * 2 / 1e6)},
+                   "parallelism": (f"ulysses-a2a x{world}" if mode == "ulysses" else f"head-parallel x{world}"),
+                   "l2": "inputs larger than L2 (%.0f MB/tensor/rank)" % (q.numel() * 2 / 1e6)},
         "kept_tflop_per_layer": f_kept_total / 1e12,
         "kept_frac": f_kept_total / dense_flops,
         "stages_ms": {"cocluster": st_cluster, "select": st_select, "permute_v_worklist": st_prep,

@@ -148,6 +148,12 @@ cs_status coclust_sparse_attention(int B, int H, int N, int d, cs_bf16_in q, cs_
                                    float scale, cs_bf16_out o, void* ws, size_t ws_bytes,
                                    void* stream, void* const* stage_events);
 
+/* Ulysses resharding helper (BASELINE configs[3]): dst[b][a] = src[a][b] for an
+ * [A, B] grid of rows of row_bytes bytes (row_bytes a multiple of 16, pointers 16-byte aligned).
+ * Packs a [N/P, H, d] token block into [P, N/P, H/P, d] per-destination chunks before the
+ * all-to-all (A = N/P, B = P, row = H/P*d) and unpacks the returned chunks after it. */
+cs_status cs_block_transpose(int A, int B, size_t row_bytes, const void* src, void* dst, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

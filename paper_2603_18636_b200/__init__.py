@@ -59,6 +59,7 @@ _SIG = {
     "coclust_sparse_attention": (_I, [_I, _I, _I, _I, _BF16In, _BF16In, _BF16In, _I, _I, _I,
                                       ctypes.c_uint64, _I, _I, _P, ctypes.c_double, ctypes.c_double, _I,
                                       ctypes.c_float, _BF16Out, _P, ctypes.c_size_t, _P, _P]),
+    "cs_block_transpose": (_I, [_I, _I, ctypes.c_size_t, _P, _P, _P]),
 }
 
 _lib = None
@@ -236,4 +237,13 @@ def coclust_sparse_attention(q, k, v, kq, kk, iters, budget, *, seed=0, tau=0.95
     _check(lib().coclust_sparse_attention(B, H, N, d, _bf16(q), _bf16(k), _bf16(v), kq, kk, iters,
                                           seed, head_offset, heads_total, _ptr(budget), float(tau), float(theta), int(rule),
                                           float(scale), _bf16(out, True), w, wn, _stream(q), evs))
+    return out
+
+
+def block_transpose(src, A, B, out=None):
+    """dst[b][a] = src[a][b] over an [A, B] grid of equal rows (Ulysses pack / unpack)."""
+    _cuda(src, "src")
+    row_bytes = src.numel() * src.element_size() // (A * B)
+    out = torch.empty(B, src.numel() // B, dtype=src.dtype, device=src.device) if out is None else out
+    _check(lib().cs_block_transpose(A, B, row_bytes, _ptr(src), _ptr(out), _stream(src)))
     return out

@@ -467,4 +467,15 @@ cs_status coclust_sparse_attention(int B, int H, int N, int d, cs_bf16_in q, cs_
                   stage_events);
 }
 
+cs_status cs_block_transpose(int A, int B, size_t row_bytes, const void* src, void* dst, void* stream) {
+  g_err[0] = 0;
+  if (A <= 0 || B <= 0 || row_bytes == 0) return fail(CS_ERR_SHAPE, "A, B, row_bytes must be positive");
+  if (row_bytes % 16) return fail(CS_ERR_ALIGN, "row_bytes must be a multiple of 16 (got %zu)", row_bytes);
+  NEED(src, "src"); NEED(dst, "dst");
+  if (reinterpret_cast<uintptr_t>(src) % 16 || reinterpret_cast<uintptr_t>(dst) % 16)
+    return fail(CS_ERR_ALIGN, "src/dst must be 16-byte aligned");
+  CS_CUDA(launch_block_transpose(A, B, row_bytes, src, dst, static_cast<cudaStream_t>(stream)), "block_transpose");
+  return CS_OK;
+}
+
 }  // extern "C"

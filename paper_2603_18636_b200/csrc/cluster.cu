@@ -412,3 +412,29 @@ cudaError_t launch_permute_rows(XView x, int BH, int N, int d, const int32_t* pe
 }
 
 }  // namespace cs
+
+namespace cs {
+// ---------------------------------------------------------------------------------------------
+// Ulysses resharding helper: dst[b][a][:] = src[a][b][:] for rows of row_bytes (a multiple of 16)
+// grid-stride over 16-byte vectors; coalesced reads and writes along the row.
+// ---------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_block_transpose(int A, int B, int vpr, const uint4* __restrict__ src,
+                                                         uint4* __restrict__ dst) {
+  const long long total = (long long)A * B * vpr;
+  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < total; i += (long long)gridDim.x * 256) {
+    const int v = (int)(i % vpr);
+    const long long ab = i / vpr;
+    const int b = (int)(ab % B), a = (int)(ab / B);
+    dst[((long long)b * A + a) * vpr + v] = src[i];
+  }
+}
+
+cudaError_t launch_block_transpose(int A, int B, size_t row_bytes, const void* src, void* dst, cudaStream_t st) {
+  const int vpr = (int)(row_bytes / 16);
+  const long long total = (long long)A * B * vpr;
+  const int grid = (int)((total + 255) / 256 < 148 * 16 ? (total + 255) / 256 : 148 * 16);
+  k_block_transpose<<<grid > 0 ? grid : 1, 256, 0, st>>>(A, B, vpr, static_cast<const uint4*>(src),
+                                                          static_cast<uint4*>(dst));
+  return cudaGetLastError();
+}
+}  // namespace cs

@@ -76,3 +76,64 @@ def test_two_rank_head_parallel_matches_single_process():
         ref = svoo.coclust_sparse_attention_head(f(w.q), f(w.k), f(w.v), 6, 10, 2, 3, 0.3, 0.95, 0.1,
                                                  svoo.RULE_DENSITY, h=h, H=H)
         assert np.array_equal(got[h], ref.O)
+
+
+def _cpu_transpose(x, A, B):
+    return x.reshape(A, B, -1).transpose(0, 1).contiguous().reshape(B, -1)
+
+
+def _oracle_layer(q, k, v, kq, kk, iters, budget, head_offset, heads_total, out=None, **kw):
+    """CPU stand-in for the CUDA layer with the same contract (global-head sampler streams)."""
+    from oracle import svoo
+    f = lambda t: t.double().numpy()
+    for h in range(q.shape[1]):
+        r = svoo.coclust_sparse_attention_head(f(q[0, h]), f(k[0, h]), f(v[0, h]), kq, kk, iters, 3,
+                                               float(budget[h]), 0.95, 0.1, svoo.RULE_DENSITY,
+                                               h=head_offset + h, H=heads_total)
+        out[0, h].copy_(torch.from_numpy(r.O))
+    return out
+
+
+def _ulysses_worker(rank, world, port, ret):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2603_18636_b200.dist import ulysses_layer
+    from synthetic import video_qkv
+    w = video_qkv(4, 8, 8, 4, 32, seed=9)            # [1, H=4, N=256, d=32]
+    N = w.q.shape[2]
+    Nl = N // world
+    blk = lambda t: t[0].permute(1, 0, 2)[rank * Nl:(rank + 1) * Nl].unsqueeze(0).double().contiguous()
+    budget = torch.tensor([0.3, 0.2, 0.5, 0.25])
+    o = ulysses_layer(blk(w.q), blk(w.k), blk(w.v), 6, 10, 2, budget, transpose=_cpu_transpose,
+                      layer=_oracle_layer)
+    gathered = [None] * world
+    dist.all_gather_object(gathered, (rank, o.numpy()))
+    if rank == 0:
+        ret.put(np.concatenate([g[1] for g in sorted(gathered, key=lambda x: x[0])], axis=1))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_ulysses_matches_single_process():
+    """Sequence-sharded inputs -> all-to-all -> per-head layer -> all-to-all back == the layer
+    run on the whole sequence in one process (same per-head sampler streams)."""
+    from oracle import svoo
+    from synthetic import video_qkv
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ulysses_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=300)          # [1, N, H, d]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    w = video_qkv(4, 8, 8, 4, 32, seed=9)
+    budget = [0.3, 0.2, 0.5, 0.25]
+    for h in range(4):
+        f = lambda t: t[0, h].double().numpy()
+        ref = svoo.coclust_sparse_attention_head(f(w.q), f(w.k), f(w.v), 6, 10, 2, 3, budget[h], 0.95, 0.1,
+                                                 svoo.RULE_DENSITY, h=h, H=4)
+        np.testing.assert_allclose(got[0, :, h, :], ref.O, atol=1e-12)
