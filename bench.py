@@ -188,6 +188,12 @@ def run_ours(args):
     c = CONFIGS[args.config]
     H_total, d = c["H"], c["d"]
     mode = args.parallel or ("ulysses" if (args.config == "hunyuan_720p" and world > 1) else "head")
+    if mode == "ulysses":
+        import torch.distributed as tdist
+        if not tdist.is_initialized():  # single-process Ulysses (P = 1): a one-rank NCCL group
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29555")
+            tdist.init_process_group("nccl", rank=0, world_size=1)
     # deterministic generation: every rank builds the full layer and keeps its share
     full = video_qkv(c["T"], c["Hs"], c["Ws"], H_total, d, seed=args.seed, device=dev)
     N = full.q.shape[2]
@@ -374,10 +380,9 @@ def main():
         run_reference(args)
     else:
         run_ours(args)
-    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
-        import torch.distributed as dist
-        if dist.is_initialized():
-            dist.destroy_process_group()
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
+        dist.destroy_process_group()
 
 
 if __name__ == "__main__":
