@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--reuse-steps", type=int, default=1,
+                    help="also time the clustering-reuse step (P:1261-1262) and report amortised ms")
     ap.add_argument("--parallel", choices=["head", "ulysses"], default=None,
                     help="multi-GPU split (default: ulysses for hunyuan_720p, head-parallel otherwise)")
     ap.add_argument("--cpu-sample-rows", type=int, default=1500,
@@ -321,6 +323,33 @@ def run_ours(args):
                "d2h_bytes_per_step": nbytes * world}
         del hq, hk, hv, ho, dq, dk, dv
 
+    # clustering reuse (NEXT-1): steps that reuse the stored clustering / selection
+    reuse = None
+    if args.reuse_steps and mode == "head":
+        st_reuse = pb.LayerState(B, H, N, d, args.kq, args.kk, dev)
+        kwc = {k_: v_ for k_, v_ in kw.items() if k_ != "out"}
+        pb.coclust_sparse_attention_cached(q, k, v, args.kq, args.kk, args.iters, budget, st_reuse, True,
+                                           out=out, **kwc)
+        for _ in range(2):
+            pb.coclust_sparse_attention_cached(q, k, v, args.kq, args.kk, args.iters, budget, st_reuse, False,
+                                               out=out, **kwc)
+        torch.cuda.synchronize()
+        a_, b2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a_.record()
+        for _ in range(K):
+            pb.coclust_sparse_attention_cached(q, k, v, args.kq, args.kk, args.iters, budget, st_reuse, False,
+                                               out=out, **kwc)
+        b2.record()
+        torch.cuda.synchronize()
+        t_reuse = a_.elapsed_time(b2) / K
+        if world > 1:
+            tt = torch.tensor([t_reuse], device=dev)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            t_reuse = float(tt[0])
+        reuse = {"reuse_step_ms": t_reuse,
+                 **{f"amortized_ms_recompute_every_{R}": (ms + (R - 1) * t_reuse) / R for R in (5, 10, 20)}}
+        del st_reuse
+
     if rank != 0:
         return
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
@@ -369,7 +398,7 @@ def run_ours(args):
                      "algorithmic": "kept FLOPs 4*d*sum_a |Q_a| sum_{c in kept[a]} |K_c| per launch (rank 0)"},
         "layer_kept_tflops": f_kept_total / (ms * 1e-3) / 1e12,
         "gpu_launches": pb.launches_per_layer(args.iters) * K,
-        "clocks": clk, "e2e": e2e, "cpu_baseline": cpu,
+        "clocks": clk, "e2e": e2e, "cpu_baseline": cpu, "clustering_reuse": reuse,
     }
     print(json.dumps(line), flush=True)
 

@@ -148,6 +148,33 @@ cs_status coclust_sparse_attention(int B, int H, int N, int d, cs_bf16_in q, cs_
                                    float scale, cs_bf16_out o, void* ws, size_t ws_bytes,
                                    void* stream, void* const* stage_events);
 
+/* Clustering-reuse state ("we reuse the clustering results and recompute them every
+ * N steps").  Caller-owned device buffers, shapes as in coclust_assign /
+ * block_select. */
+typedef struct {
+  float* cq;       /* [B,H,kq,d] */
+  float* ck;       /* [B,H,kk,d] */
+  int32_t* lq;     /* [B,H,N]    */
+  int32_t* lk;     /* [B,H,N]    */
+  int32_t* perm_q; /* [B,H,N]    */
+  int32_t* perm_k; /* [B,H,N]    */
+  int32_t* offs_q; /* [B,H,kq+1] */
+  int32_t* offs_k; /* [B,H,kk+1] */
+  int32_t* n_keep; /* [B,H]      */
+  int32_t* kept;   /* [B,H,kq,kk]*/
+} cs_layer_state;
+
+/* coclust_sparse_attention with caller-owned state: recompute != 0 runs co-clustering and selection
+ * and stores them in *state; recompute == 0 skips both and reuses *state (only Q, K, V are
+ * re-permuted), so a caller recomputes every R_reuse denoising steps (R14). */
+cs_status coclust_sparse_attention_cached(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in k,
+                                          cs_bf16_in v, int kq, int kk, int iters, uint64_t seed,
+                                          int head_offset, int heads_total, const float* budget,
+                                          double tau, double theta, int rule, float scale,
+                                          cs_bf16_out o, const cs_layer_state* state, int recompute,
+                                          void* ws, size_t ws_bytes, void* stream,
+                                          void* const* stage_events);
+
 /* Ulysses resharding helper (BASELINE configs[3]): dst[b][a] = src[a][b] for an
  * [A, B] grid of rows of row_bytes bytes (row_bytes a multiple of 16, pointers 16-byte aligned).
  * Packs a [N/P, H, d] token block into [P, N/P, H/P, d] per-destination chunks before the

@@ -60,6 +60,10 @@ _SIG = {
                                       ctypes.c_uint64, _I, _I, _P, ctypes.c_double, ctypes.c_double, _I,
                                       ctypes.c_float, _BF16Out, _P, ctypes.c_size_t, _P, _P]),
     "cs_block_transpose": (_I, [_I, _I, ctypes.c_size_t, _P, _P, _P]),
+    "coclust_sparse_attention_cached": (_I, [_I, _I, _I, _I, _BF16In, _BF16In, _BF16In, _I, _I, _I,
+                                             ctypes.c_uint64, _I, _I, _P, ctypes.c_double, ctypes.c_double,
+                                             _I, ctypes.c_float, _BF16Out, _P, _I, _P, ctypes.c_size_t, _P,
+                                             _P]),
 }
 
 _lib = None
@@ -246,4 +250,47 @@ def block_transpose(src, A, B, out=None):
     row_bytes = src.numel() * src.element_size() // (A * B)
     out = torch.empty(B, src.numel() // B, dtype=src.dtype, device=src.device) if out is None else out
     _check(lib().cs_block_transpose(A, B, row_bytes, _ptr(src), _ptr(out), _stream(src)))
+    return out
+
+
+class _LayerState(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in ("cq", "ck", "lq", "lk", "perm_q", "perm_k", "offs_q",
+                                               "offs_k", "n_keep", "kept")]
+
+
+class LayerState:
+    """Device buffers of the clustering-reuse state (cs_layer_state) for one layer."""
+
+    def __init__(self, B, H, N, d, kq, kk, device):
+        i32 = dict(dtype=torch.int32, device=device)
+        self.cq = torch.empty(B, H, kq, d, dtype=torch.float32, device=device)
+        self.ck = torch.empty(B, H, kk, d, dtype=torch.float32, device=device)
+        self.lq, self.lk = torch.empty(B, H, N, **i32), torch.empty(B, H, N, **i32)
+        self.perm_q, self.perm_k = torch.empty(B, H, N, **i32), torch.empty(B, H, N, **i32)
+        self.offs_q = torch.empty(B, H, kq + 1, **i32)
+        self.offs_k = torch.empty(B, H, kk + 1, **i32)
+        self.n_keep = torch.empty(B, H, **i32)
+        self.kept = torch.empty(B, H, kq, kk, **i32)
+        self._c = _LayerState(*[t.data_ptr() for t in (self.cq, self.ck, self.lq, self.lk, self.perm_q,
+                                                        self.perm_k, self.offs_q, self.offs_k, self.n_keep,
+                                                        self.kept)])
+
+
+def coclust_sparse_attention_cached(q, k, v, kq, kk, iters, budget, state, recompute, *, seed=0, tau=0.95,
+                                    theta=0.1, rule=RULE_DENSITY, scale=None, out=None, ws=None,
+                                    head_offset=0, heads_total=0, stage_events=None):
+    """The layer with clustering reuse: recompute=True refreshes `state`."""
+    _cuda(q, "q")
+    B, H, N, d = q.shape
+    scale = d ** -0.5 if scale is None else scale
+    out = torch.empty(B, H, N, d, dtype=torch.bfloat16, device=q.device) if out is None else out
+    w, wn = _ws(ws, workspace_bytes(B, H, N, d, kq, kk), q.device)
+    evs = None
+    if stage_events is not None:
+        evs = (ctypes.c_void_p * 4)(*[ctypes.c_void_p(e.cuda_event) for e in stage_events])
+    _check(lib().coclust_sparse_attention_cached(B, H, N, d, _bf16(q), _bf16(k), _bf16(v), kq, kk, iters,
+                                                 seed, head_offset, heads_total, _ptr(budget), float(tau),
+                                                 float(theta), int(rule), float(scale), _bf16(out, True),
+                                                 ctypes.byref(state._c), int(bool(recompute)), w, wn,
+                                                 _stream(q), evs))
     return out

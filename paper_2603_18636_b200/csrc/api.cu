@@ -427,12 +427,12 @@ cs_status block_sparse_attn(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in
   return run_attn(B, H, N, d, kq, kk, perm_q, offs_q, offs_k, n_keep, kept, scale, o, sc, st);
 }
 
-cs_status coclust_sparse_attention(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in k, cs_bf16_in v, int kq,
-                                   int kk, int iters, uint64_t seed, int head_offset, int heads_total,
-                                   const float* budget, double tau, double theta,
-                                   int rule, float scale, cs_bf16_out o, void* ws, size_t ws_bytes, void* stream,
-                                   void* const* stage_events) {
-  g_err[0] = 0;
+}  // extern "C"
+
+namespace {
+cs_status check_layer_args(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in k, cs_bf16_in v, int kq, int kk,
+                           int iters, int& head_offset, int& heads_total, const float* budget, double tau,
+                           double theta, int rule, float scale, cs_bf16_out o) {
   CS_CHECK(check_dims(B, H, N, d));
   CS_CHECK(check_k(kq, N, "kq"));
   CS_CHECK(check_k(kk, N, "kk"));
@@ -447,24 +447,80 @@ cs_status coclust_sparse_attention(int B, int H, int N, int d, cs_bf16_in q, cs_
   CS_CHECK(check_bf16(v.ptr, v.sb, v.sh, v.sn, "v"));
   CS_CHECK(check_bf16(o.ptr, o.sb, o.sh, o.sn, "o"));
   NEED(budget, "budget");
+  return CS_OK;
+}
+
+// The whole layer on device.  recompute: co-cluster + select into `s`; otherwise reuse `s`.
+cs_status run_layer(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in k, cs_bf16_in v, int kq, int kk,
+                    int iters, uint64_t seed, int head_offset, int heads_total, const float* budget, double tau,
+                    double theta, int rule, float scale, cs_bf16_out o, const LayerState& s, bool recompute,
+                    Carve& c, cudaStream_t st, void* const* ev) {
+  const int BH = B * H;
+  AttnScratch at = carve_attn(c, BH, N, d, kq);
+  AssignScratch as = carve_assign(c, BH, N, d, kq, kk);
+  SelectScratch se = carve_select(c, BH, kq, kk);
+  if (recompute) {
+    CS_CHECK(run_assign(B, H, N, d, q, k, kq, kk, iters, seed, head_offset, heads_total, nullptr, nullptr, s.cq,
+                        s.ck, s.lq, s.lk, s.perm_q, s.offs_q, s.perm_k, s.offs_k, as, at.qp, at.kp, st));
+    if (ev) CS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(ev[0]), st), "event");
+    CS_CUDA(launch_block_select(BH, H, kq, kk, d, s.cq, s.ck, s.offs_q, s.offs_k, budget, tau, theta, rule,
+                                s.n_keep, s.kept, se.order, se.cnt, se.abar, st),
+            "block_select");
+    if (ev) CS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(ev[1]), st), "event");
+  } else {
+    // clustering reuse across denoising steps: only the permuted copies are new
+    if (ev) CS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(ev[0]), st), "event");
+    CS_CUDA(launch_permute_rows(view(q, H), BH, N, d, s.perm_q, at.qp, st), "permute_q");
+    CS_CUDA(launch_permute_rows(view(k, H), BH, N, d, s.perm_k, at.kp, st), "permute_k");
+    if (ev) CS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(ev[1]), st), "event");
+  }
+  CS_CUDA(launch_permute_rows(view(v, H), BH, N, d, s.perm_k, at.vp, st), "permute_v");
+  return run_attn(B, H, N, d, kq, kk, s.perm_q, s.offs_q, s.offs_k, s.n_keep, s.kept, scale, o, at, st, ev);
+}
+}  // namespace
+
+extern "C" {
+
+cs_status coclust_sparse_attention(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in k, cs_bf16_in v, int kq,
+                                   int kk, int iters, uint64_t seed, int head_offset, int heads_total,
+                                   const float* budget, double tau, double theta,
+                                   int rule, float scale, cs_bf16_out o, void* ws, size_t ws_bytes, void* stream,
+                                   void* const* stage_events) {
+  g_err[0] = 0;
+  CS_CHECK(check_layer_args(B, H, N, d, q, k, v, kq, kk, iters, head_offset, heads_total, budget, tau, theta,
+                            rule, scale, o));
   const int BH = B * H;
   CS_CHECK(check_ws(ws, ws_bytes, need_layer(BH, N, d, kq, kk)));
   Carve c(ws);
   LayerState s = carve_state(c, BH, N, d, kq, kk);
-  AttnScratch at = carve_attn(c, BH, N, d, kq);
-  AssignScratch as = carve_assign(c, BH, N, d, kq, kk);
-  SelectScratch se = carve_select(c, BH, kq, kk);
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  CS_CHECK(run_assign(B, H, N, d, q, k, kq, kk, iters, seed, head_offset, heads_total, nullptr, nullptr, s.cq, s.ck, s.lq, s.lk, s.perm_q,
-                      s.offs_q, s.perm_k, s.offs_k, as, at.qp, at.kp, st));
-  if (stage_events) CS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(stage_events[0]), st), "event");
-  CS_CUDA(launch_block_select(BH, H, kq, kk, d, s.cq, s.ck, s.offs_q, s.offs_k, budget, tau, theta, rule,
-                              s.n_keep, s.kept, se.order, se.cnt, se.abar, st),
-          "block_select");
-  if (stage_events) CS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(stage_events[1]), st), "event");
-  CS_CUDA(launch_permute_rows(view(v, H), BH, N, d, s.perm_k, at.vp, st), "permute_v");
-  return run_attn(B, H, N, d, kq, kk, s.perm_q, s.offs_q, s.offs_k, s.n_keep, s.kept, scale, o, at, st,
-                  stage_events);
+  return run_layer(B, H, N, d, q, k, v, kq, kk, iters, seed, head_offset, heads_total, budget, tau, theta, rule,
+                   scale, o, s, true, c, static_cast<cudaStream_t>(stream), stage_events);
+}
+
+cs_status coclust_sparse_attention_cached(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in k, cs_bf16_in v,
+                                          int kq, int kk, int iters, uint64_t seed, int head_offset,
+                                          int heads_total, const float* budget, double tau, double theta, int rule,
+                                          float scale, cs_bf16_out o, const cs_layer_state* state, int recompute,
+                                          void* ws, size_t ws_bytes, void* stream, void* const* stage_events) {
+  g_err[0] = 0;
+  CS_CHECK(check_layer_args(B, H, N, d, q, k, v, kq, kk, iters, head_offset, heads_total, budget, tau, theta,
+                            rule, scale, o));
+  NEED(state, "state");
+  NEED(state->cq, "state->cq"); NEED(state->ck, "state->ck"); NEED(state->lq, "state->lq");
+  NEED(state->lk, "state->lk"); NEED(state->perm_q, "state->perm_q"); NEED(state->offs_q, "state->offs_q");
+  NEED(state->perm_k, "state->perm_k"); NEED(state->offs_k, "state->offs_k");
+  NEED(state->n_keep, "state->n_keep"); NEED(state->kept, "state->kept");
+  const int BH = B * H;
+  Carve dry(nullptr);
+  carve_attn(dry, BH, N, d, kq);
+  carve_assign(dry, BH, N, d, kq, kk);
+  carve_select(dry, BH, kq, kk);
+  CS_CHECK(check_ws(ws, ws_bytes, dry.off + 256));
+  LayerState s{state->cq, state->ck, state->lq, state->lk, state->perm_q, state->perm_k, state->offs_q,
+               state->offs_k, state->n_keep, state->kept};
+  Carve c(ws);
+  return run_layer(B, H, N, d, q, k, v, kq, kk, iters, seed, head_offset, heads_total, budget, tau, theta, rule,
+                   scale, o, s, recompute != 0, c, static_cast<cudaStream_t>(stream), stage_events);
 }
 
 cs_status cs_block_transpose(int A, int B, size_t row_bytes, const void* src, void* dst, void* stream) {

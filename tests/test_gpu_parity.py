@@ -334,3 +334,33 @@ def test_determinism_and_head_sharding(pb):
         o3 = pb.coclust_sparse_attention(q[:, sl].contiguous(), k[:, sl].contiguous(), v[:, sl].contiguous(),
                                          20, 60, 2, budget[sl].contiguous(), head_offset=2 * r, heads_total=4)
         assert torch.equal(o3, o1[:, sl])
+
+
+def test_clustering_reuse_cached_entry(pb):
+    """NEXT-1: recompute=True == the fused layer and fills the state; recompute=False
+    reuses the stored labels / kept blocks on new inputs (checked against the oracle)."""
+    w = video_qkv(4, 16, 24, 2, 128, seed=6)
+    q, k, v = w.q.cuda(), w.k.cuda(), w.v.cuda()
+    budget = torch.tensor([0.25, 0.35], dtype=torch.float32).cuda()
+    B, H, N, d = q.shape
+    st = pb.LayerState(B, H, N, d, 24, 64, q.device)
+    o_full = pb.coclust_sparse_attention(q, k, v, 24, 64, 2, budget)
+    o_rec = pb.coclust_sparse_attention_cached(q, k, v, 24, 64, 2, budget, st, True)
+    ref = pb.coclust_assign(q, k, 24, 64, 2)
+    torch.cuda.synchronize()
+    assert torch.equal(o_full, o_rec)
+    for key in ("lq", "lk", "perm_q", "offs_q", "perm_k", "offs_k"):
+        assert torch.equal(getattr(st, key), ref[key]), key
+    o_same = pb.coclust_sparse_attention_cached(q, k, v, 24, 64, 2, budget, st, False)
+    assert torch.equal(o_same, o_full)
+    g = torch.Generator(device="cuda").manual_seed(1)
+    q2 = (q.float() + 0.05 * torch.randn(q.shape, generator=g, device="cuda")).to(torch.bfloat16)
+    v2 = (v.float() + 0.05 * torch.randn(v.shape, generator=g, device="cuda")).to(torch.bfloat16)
+    o2 = pb.coclust_sparse_attention_cached(q2, k, v2, 24, 64, 2, budget, st, False)
+    torch.cuda.synchronize()
+    for h in range(H):
+        n = int(st.n_keep[0, h])
+        ref_o = svoo.sparse_attention(f64(q2[0, h]), f64(k[0, h]), f64(v2[0, h]), st.lq[0, h].cpu().numpy(),
+                                      st.lk[0, h].cpu().numpy(), st.kept[0, h, :, :n].cpu().numpy())
+        err = np.abs(f64(o2[0, h]) - ref_o)
+        assert err.max() <= ATOL_MAX and err.mean() <= ATOL_MEAN
