@@ -245,6 +245,11 @@ CS_DEV float2 ex2_poly2(float2 x) {
   return make_float2(__int_as_float(__float_as_int(p.x) + ex), __int_as_float(__float_as_int(p.y) + ey));
 }
 
+// named barrier over `count` threads (multiple of 32), id 1..15 (0 is __syncthreads)
+CS_DEV void named_bar_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
 template <typename T>
 CS_DEV T warp_sum(T v) {
 #pragma unroll
