@@ -53,8 +53,8 @@ struct Smem {
   static constexpr int OFF_K = OFF_Q + 2 * QT;
   static constexpr int OFF_V = OFF_K + NST * KT;
   static constexpr int OFF_BAR = OFF_V + NST * KT;
-  // q_full, k_full[2], k_empty[2], v_full[2], v_empty[2], s_full[2], p_full[2], o_full
-  static constexpr int OFF_MISC = OFF_BAR + 8 * 16;  // tmem slot, U, n
+  // q_full, k_full[2], k_empty[2], v_full[2], v_empty[2], s_full[2], p_full[2 tiles][2 halves], o_full
+  static constexpr int OFF_MISC = OFF_BAR + 16 * 8;  // tmem slot, U, n
   static constexpr int OFF_UROW = OFF_MISC + 16;      // [NST][UPT] unit start rows
   static constexpr int OFF_KSTART = OFF_UROW + NST * UPT * 4;
   static constexpr int OFF_KLEN = OFF_KSTART + kMaxClusters * 4;
@@ -82,8 +82,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint64_t* v_full = bars + 5;
   uint64_t* v_empty = bars + 7;
   uint64_t* s_full = bars + 9;
-  uint64_t* p_full = bars + 11;
-  uint64_t* o_full = bars + 13;
+  uint64_t* p_full = bars + 11;  // [tq * 2 + half]: P columns of keys [64 half, 64 half + 64)
+  uint64_t* o_full = bars + 15;
   int* misc = reinterpret_cast<int*>(sm + L::OFF_MISC);
   int* kstart = reinterpret_cast<int*>(sm + L::OFF_KSTART);
   int* klen = reinterpret_cast<int*>(sm + L::OFF_KLEN);
@@ -114,7 +114,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       mbar_init(k_full + s, 1); mbar_init(k_empty + s, 1);
       mbar_init(v_full + s, 1); mbar_init(v_empty + s, 1);
     }
-    for (int t = 0; t < 2; ++t) { mbar_init(s_full + t, 1); mbar_init(p_full + t, 128); }
+    for (int t = 0; t < 2; ++t) mbar_init(s_full + t, 1);
+    for (int t = 0; t < 4; ++t) mbar_init(p_full + t, 128);
     mbar_init(o_full, 1);
     fence_barrier_init();
   }
@@ -235,16 +236,27 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
       __syncwarp();
     };
-    auto issue_pv = [&](int tq, int slot, bool acc) {
+    // PV over the keys [64 half, 64 half + 64) of V slot `slot` (4 K-steps of 16 keys)
+    auto issue_pv = [&](int tq, int slot, int half, bool acc) {
       if (elect_one()) {
         const uint32_t d_tmem = tmem + 256 + tq * 128;
         const uint32_t p_tmem = tmem + tq * 128;
         const uint64_t vd = dv0 + (uint64_t)((slot * L::KT) >> 4);
 #pragma unroll
-        for (int kk2 = 0; kk2 < BN / 16; ++kk2)
+        for (int k4 = 0; k4 < BN / 32; ++k4) {
+          const int kk2 = half * (BN / 32) + k4;
           mma_ts(d_tmem, p_tmem + kk2 * 8, vd + (uint64_t)((kk2 * 2048) >> 4), idesc_pv, (acc || kk2 > 0) ? 1u : 0u);
+        }
       }
       __syncwarp();
+    };
+    auto wait_pv = [&](int tq, int slot, int j) {
+      mbar_wait(p_full + tq * 2 + 0, j & 1);
+      tc_fence_after();
+      issue_pv(tq, slot, 0, j > 0);
+      mbar_wait(p_full + tq * 2 + 1, j & 1);
+      tc_fence_after();
+      issue_pv(tq, slot, 1, true);
     };
     auto commit = [&](uint64_t* bar) {
       if (elect_one()) mma_commit(bar);
@@ -260,12 +272,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     for (int j = 0; j < nt; ++j) {
       const int slot = j % NST, slot1 = (j + 1) % NST;
       const bool more = j + 1 < nt;
-      mbar_wait(p_full + 0, j & 1);
-      CS_TRACE(4, j);
       mbar_wait(v_full + slot, (j / NST) & 1);
       CS_TRACE(3, j);
-      tc_fence_after();
-      issue_pv(0, slot, j > 0);
+      wait_pv(0, slot, j);
+      CS_TRACE(4, j);
       if (more) {
         mbar_wait(k_full + slot1, ((j + 1) / NST) & 1);
         CS_TRACE(2, j + 1);
@@ -274,10 +284,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         commit(s_full + 0);
       }
       if (has1) {
-        mbar_wait(p_full + 1, j & 1);
+        wait_pv(1, slot, j);
         CS_TRACE(11, j);
-        tc_fence_after();
-        issue_pv(1, slot, j > 0);
       }
       commit(v_empty + slot);
       if (more) {
@@ -371,45 +379,46 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           l *= alpha;
           m = mx;
         }
-        // tcgen05.ld/st are warp-collective (.sync.aligned): rescale if any row of the warp needs it
         const bool warp_rescale = __any_sync(0xffffffffu, alpha != 1.f);
-        // p = 2^(s*scale_log2 - m): paired FFMA2, MUFU ex2, 4 independent FADD2 row-sum chains
+        // p = 2^(s*scale_log2 - m): paired FFMA2, MUFU ex2, 4 independent FADD2 row-sum chains.
+        // Each 64-key half of P is stored and signalled as soon as it is done, so PV on the
+        // first half overlaps the exponentials of the second.
         const float2 sl2 = make_float2(scale_log2, scale_log2), nm2 = make_float2(-m, -m);
         float2 acc4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
-        for (int c = 0; c < BN; c += 2) {
-#ifdef CS_EXP_OLD
-          const float2 x = make_float2(__uint_as_float(su[c]) * scale_log2 - m, __uint_as_float(su[c + 1]) * scale_log2 - m);
-#else
-          const float2 x = ffma2(make_float2(__uint_as_float(su[c]), __uint_as_float(su[c + 1])), sl2, nm2);
-#endif
-          // every 4th pair on the FMA pipe (polynomial), the rest on MUFU: keeps MUFU below the
-          // tensor-core time of the two ping-ponged tiles
-          const float2 p = (kPolyEvery > 0 && ((c >> 1) % kPolyEvery) == kPolyEvery - 1)
-                               ? ex2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
-          acc4[(c >> 1) & 3] = fadd2(acc4[(c >> 1) & 3], p);
-          su[c >> 1] = pack_bf16x2(p.x, p.y);
+        for (int hf = 0; hf < 2; ++hf) {
+#pragma unroll
+          for (int c = hf * (BN / 2); c < (hf + 1) * (BN / 2); c += 2) {
+            const float2 x = ffma2(make_float2(__uint_as_float(su[c]), __uint_as_float(su[c + 1])), sl2, nm2);
+            // every kPolyEvery-th pair on the FMA pipe (polynomial), the rest on MUFU: keeps
+            // MUFU below the tensor-core time of the two ping-ponged tiles
+            const float2 p = (kPolyEvery > 0 && ((c >> 1) % kPolyEvery) == kPolyEvery - 1)
+                                 ? ex2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
+            acc4[(c >> 1) & 3] = fadd2(acc4[(c >> 1) & 3], p);
+            su[c >> 1] = pack_bf16x2(p.x, p.y);
+          }
+          tmem_st32(s_tm + hf * 32, su + hf * 32);
+          // lazy O rescale before PV(j) starts (it waits for p_full(j, half 0)).  tcgen05.ld/st
+          // are warp-collective, so the warp rescales if any of its rows needs it.  O is stable:
+          // PV(j-1) completed before s_full(j) (same commit order).
+          if (hf == 0 && warp_rescale) {
+#pragma unroll 1
+            for (int c = 0; c < D / 16; ++c) {
+              uint32_t ov[16];
+              tmem_ld16(o_tm + c * 16, ov);
+              tmem_wait_ld();
+#pragma unroll
+              for (int i = 0; i < 16; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
+              tmem_st16(o_tm + c * 16, ov);
+            }
+          }
+          tmem_wait_st();
+          tc_fence_before();
+          mbar_arrive(p_full + tq * 2 + hf);
         }
         const float2 s01 = fadd2(acc4[0], acc4[1]), s23 = fadd2(acc4[2], acc4[3]);
         const float2 s4 = fadd2(s01, s23);
         l += s4.x + s4.y;
-        CS_TRACE(14 + tq, j);
-        tmem_st32(s_tm, su);
-        tmem_st32(s_tm + 32, su + 32);
-        if (warp_rescale) {  // lazy O rescale; PV(j) is not issued before p_full(j)
-#pragma unroll 1
-          for (int c = 0; c < D / 32; ++c) {
-            uint32_t ov[32];
-            tmem_ld32(o_tm + c * 32, ov);
-            tmem_wait_ld();
-#pragma unroll
-            for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
-            tmem_st32(o_tm + c * 32, ov);
-          }
-        }
-        tmem_wait_st();
-        tc_fence_before();
-        mbar_arrive(p_full + tq);
         CS_TRACE(6 + 2 * tq, j);
         if (j + 1 < nt) tile_mask(j + 1);
       }
