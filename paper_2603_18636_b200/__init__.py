@@ -227,9 +227,10 @@ def block_sparse_attn(q, k, v, perm_q, offs_q, perm_k, offs_k, n_keep, kept, sca
 def coclust_sparse_attention(q, k, v, kq, kk, iters, budget, *, seed=0, tau=0.95, theta=0.1,
                              rule=RULE_DENSITY, scale=None, out=None, ws=None, head_offset=0,
                              heads_total=0, stage_events=None):
-    """stage_events: optional 4 torch.cuda.Event (enable_timing) recorded after co-clustering,
+    """The whole SVOO attention layer (north_star stages 1-5) on device.
+
+    stage_events: optional 4 torch.cuda.Event (enable_timing) recorded after co-clustering,
     after selection, and around the attention kernel."""
-    """The whole SVOO attention layer (north_star stages 1-5) on device."""
     _cuda(q, "q")
     B, H, N, d = q.shape
     scale = d ** -0.5 if scale is None else scale

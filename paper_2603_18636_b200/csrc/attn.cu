@@ -8,8 +8,9 @@
 // rows, one 1 KB SWIZZLE_128B atom per 8 rows), so padding is < 8 rows per kept cluster.  Rows of
 // a cluster's last unit past its end are masked to -inf in the softmax.
 //
-// Warp roles (320 threads):  warps 0-3 softmax/epilogue of Q tile 0 (TMEM lanes 0-127),
-// warps 4-7 the same for Q tile 1, warp 8 TMA producer, warp 9 TMEM allocator + MMA issuer.
+// Warp roles (352 threads):  warps 0-3 softmax/epilogue of Q tile 0 (TMEM lanes 0-127),
+// warps 4-7 the same for Q tile 1, warp 8 TMA producer (Q, K), warp 9 TMEM allocator + MMA
+// issuer, warp 10 TMA producer (V).
 // TMEM (512 cols): S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512); P (bf16x2) overwrites the
 // first 64 columns of its S buffer and feeds the PV MMA from TMEM (A operand), V from SMEM
 // (MN-major).  K and V have separate 2-slot rings: K(j) is released as soon as both QK(j) MMAs
@@ -59,7 +60,8 @@ struct Smem {
   static constexpr int OFF_KSTART = OFF_UROW + NST * UPT * 4;
   static constexpr int OFF_KLEN = OFF_KSTART + kMaxClusters * 4;
   static constexpr int OFF_UCUM = OFF_KLEN + kMaxClusters * 4;
-  static constexpr int BYTES = OFF_UCUM + (kMaxClusters + 1) * 4;
+  static constexpr int OFF_XCH = OFF_UCUM + ((kMaxClusters + 1) * 4 + 15) / 16 * 16;
+  static constexpr int BYTES = OFF_XCH + 4 * BM * 4;  // split-KV merge: m[2][BM], l[2][BM]
   static constexpr int ALLOC = BYTES + 1024;  // room to align the base to 1024
 };
 
@@ -88,6 +90,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   int* kstart = reinterpret_cast<int*>(sm + L::OFF_KSTART);
   int* klen = reinterpret_cast<int*>(sm + L::OFF_KLEN);
   int* ucum = reinterpret_cast<int*>(sm + L::OFF_UCUM);
+  float* xch = reinterpret_cast<float*>(sm + L::OFF_XCH);
 
   const int bh = blockIdx.y;
   const int item = blockIdx.x;
@@ -105,6 +108,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const int qlen = offs_q[(size_t)bh * (kq + 1) + a + 1] - qbeg;
   const int t0 = 2 * pair;
   const bool has1 = (t0 + 1) * BM < qlen;
+  // single-tile item: split the KV sequence between the two accumulator sets (even / odd KV
+  // tiles) so the softmax of one still overlaps the MMAs of the other; merged in the epilogue
+  const bool split = !has1;
   const int warp = warp_id(), lane = lane_id();
 
   // ---- setup: barriers (thread 0), TMEM (warp 9), unit table (warp 8)
@@ -222,10 +228,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const uint64_t dq0 = smem_desc_sw128(smem_u32(sm + L::OFF_Q), 16, 1024);
     const uint64_t dk0 = smem_desc_sw128(smem_u32(sm + L::OFF_K), 16, 1024);
     const uint64_t dv0 = smem_desc_sw128(smem_u32(sm + L::OFF_V), L::HALF_K, 1024);
-    auto issue_qk = [&](int tq, int slot) {
+    auto issue_qk = [&](int tq, int slot, int qs) {  // S[tq] = Q slot qs x K slot `slot`
       if (elect_one()) {
         const uint32_t d_tmem = tmem + tq * 128;
-        const uint64_t qd = dq0 + (uint64_t)((tq * L::QT) >> 4);
+        const uint64_t qd = dq0 + (uint64_t)((qs * L::QT) >> 4);
         const uint64_t kd = dk0 + (uint64_t)((slot * L::KT) >> 4);
 #pragma unroll
         for (int kk2 = 0; kk2 < D / 16; ++kk2) {
@@ -263,41 +269,87 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       __syncwarp();
     };
     mbar_wait(q_full, 0);
-    mbar_wait(k_full, 0);
-    tc_fence_after();
-    issue_qk(0, 0);
-    commit(s_full + 0);
-    if (has1) { issue_qk(1, 0); commit(s_full + 1); }
-    commit(k_empty + 0);
-    for (int j = 0; j < nt; ++j) {
-      const int slot = j % NST, slot1 = (j + 1) % NST;
-      const bool more = j + 1 < nt;
-      mbar_wait(v_full + slot, (j / NST) & 1);
-      CS_TRACE(3, j);
-      wait_pv(0, slot, j);
-      CS_TRACE(4, j);
-      if (more) {
-        mbar_wait(k_full + slot1, ((j + 1) / NST) & 1);
-        CS_TRACE(2, j + 1);
+    if (!split) {
+      // two Q tiles share every K/V tile.  Per KV tile j: PV0(j), QK0(j+1), PV1(j), QK1(j+1).
+      mbar_wait(k_full, 0);
+      tc_fence_after();
+      issue_qk(0, 0, 0);
+      commit(s_full + 0);
+      if (has1) { issue_qk(1, 0, 1); commit(s_full + 1); }
+      commit(k_empty + 0);
+      for (int j = 0; j < nt; ++j) {
+        const int slot = j % NST, slot1 = (j + 1) % NST;
+        const bool more = j + 1 < nt;
+        mbar_wait(v_full + slot, (j / NST) & 1);
+        CS_TRACE(3, j);
+        wait_pv(0, slot, j);
+        CS_TRACE(4, j);
+        if (more) {
+          mbar_wait(k_full + slot1, ((j + 1) / NST) & 1);
+          CS_TRACE(2, j + 1);
+          tc_fence_after();
+          issue_qk(0, slot1, 0);
+          commit(s_full + 0);
+        }
+        if (has1) {
+          wait_pv(1, slot, j);
+          CS_TRACE(11, j);
+        }
+        commit(v_empty + slot);
+        if (more) {
+          if (has1) { issue_qk(1, slot1, 1); commit(s_full + 1); }
+          commit(k_empty + slot1);
+        }
+      }
+    } else {
+      // split-KV: one Q tile (slot 0); accumulator set tq takes the KV tiles 2j + tq, which the
+      // producers place in ring slot tq (use j of the slot -> parity j & 1).  Same ping-pong:
+      // PV0(2j), QK0(2j+2), PV1(2j+1), QK1(2j+3).
+      mbar_wait(k_full + 0, 0);
+      tc_fence_after();
+      issue_qk(0, 0, 0);
+      commit(s_full + 0);
+      commit(k_empty + 0);
+      if (nt > 1) {
+        mbar_wait(k_full + 1, 0);
         tc_fence_after();
-        issue_qk(0, slot1);
-        commit(s_full + 0);
+        issue_qk(1, 1, 0);
+        commit(s_full + 1);
+        commit(k_empty + 1);
       }
-      if (has1) {
-        wait_pv(1, slot, j);
-        CS_TRACE(11, j);
-      }
-      commit(v_empty + slot);
-      if (more) {
-        if (has1) { issue_qk(1, slot1); commit(s_full + 1); }
-        commit(k_empty + slot1);
+      for (int j = 0; 2 * j < nt; ++j) {
+        const bool has_b = 2 * j + 1 < nt, more_a = 2 * j + 2 < nt, more_b = 2 * j + 3 < nt;
+        mbar_wait(v_full + 0, j & 1);
+        wait_pv(0, 0, j);
+        commit(v_empty + 0);
+        if (more_a) {
+          mbar_wait(k_full + 0, (j + 1) & 1);
+          tc_fence_after();
+          issue_qk(0, 0, 0);
+          commit(s_full + 0);
+          commit(k_empty + 0);
+        }
+        if (has_b) {
+          mbar_wait(v_full + 1, j & 1);
+          wait_pv(1, 1, j);
+          commit(v_empty + 1);
+          if (more_b) {
+            mbar_wait(k_full + 1, (j + 1) & 1);
+            tc_fence_after();
+            issue_qk(1, 1, 0);
+            commit(s_full + 1);
+            commit(k_empty + 1);
+          }
+        }
       }
     }
     commit(o_full);
   } else {
     // ================= softmax / epilogue (warps 0-7) =================
     const int tq = warp >> 2;
-    if (tq == 0 || has1) {
+    // KV tiles of this accumulator set: all of them, or every other one (from tq) when split
+    const int my_nt = split ? (nt + 1 - tq) / 2 : nt;
+    if (my_nt > 0) {
       const int quad = warp & 3;
       const int r = quad * 32 + lane;  // row of the Q tile == TMEM lane
       const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
@@ -316,7 +368,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           const int gl = ucum[ci + 1] - 1;  // last unit of kept cluster ci
           if (gl >= g0 + UPT) break;
           const int vc = klen[ci] - UNIT * (gl - ucum[ci]);
-          if (vc < UNIT && gl >= ucum[ci]) {
+          if (vc < UNIT && gl >= ucum[ci] && gl >= g0) {  // (split: may end in a skipped tile)
             const int u = gl - g0;
             const uint32_t bits = ((0xffu << vc) & 0xffu) << (8 * (u & 3));
             const int w = u >> 2;
@@ -338,8 +390,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       float dbg_s0_keep = 0.f, dbg_s1_keep = 0.f;
       uint32_t dbg_mw0_keep = 0;
 #endif
-      tile_mask(0);
-      for (int j = 0; j < nt; ++j) {
+      tile_mask(split ? tq : 0);
+      for (int j = 0; j < my_nt; ++j) {
         mbar_wait(s_full + tq, j & 1);
         CS_TRACE(5 + 2 * tq, j);
         tc_fence_after();
@@ -415,42 +467,69 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           tmem_wait_st();
           tc_fence_before();
           mbar_arrive(p_full + tq * 2 + hf);
+          if (hf == 0) CS_TRACE(14 + tq, j);
         }
         const float2 s01 = fadd2(acc4[0], acc4[1]), s23 = fadd2(acc4[2], acc4[3]);
         const float2 s4 = fadd2(s01, s23);
         l += s4.x + s4.y;
         CS_TRACE(6 + 2 * tq, j);
-        if (j + 1 < nt) tile_mask(j + 1);
+        if (j + 1 < my_nt) tile_mask(split ? 2 * (j + 1) + tq : j + 1);
       }
       // ---- epilogue: O / l -> bf16, scattered to original token order
       mbar_wait(o_full, 0);
       tc_fence_after();
-      const int prow = (t0 + tq) * BM + r;
+      const int prow = (t0 + (split ? 0 : tq)) * BM + r;
       const bool row_ok = prow < qlen;
-      const float inv_l = 1.f / l;
       const int tok = row_ok ? perm_q[(size_t)bh * N + qbeg + prow] : 0;
       const int b = bh / H, h = bh % H;
       __nv_bfloat16* dst = out + (long long)b * osb + (long long)h * osh + (long long)tok * osn;
+      if (split && nt > 1) {
+        // merge the two partial states of the row (each relative to its own running max):
+        // O = (O0 2^(m0-M) + O1 2^(m1-M)) / (l0 2^(m0-M) + l1 2^(m1-M)); set tq writes the
+        // output columns [tq D/2, (tq+1) D/2)
+        xch[tq * BM + r] = m;
+        xch[(2 + tq) * BM + r] = l;
+        named_bar_sync(1, 256);
+        const float m0 = xch[r], m1 = xch[BM + r];
+        const float M = fmaxf(m0, m1);
+        const float a0 = ex2(m0 - M), a1 = ex2(m1 - M);
+        const float inv = 1.f / (xch[2 * BM + r] * a0 + xch[3 * BM + r] * a1);
+        const float f0 = a0 * inv, f1 = a1 * inv;
+        const uint32_t o0 = tmem + lane_off + 256, o1 = tmem + lane_off + 384;
+#pragma unroll 1
+        for (int c0 = 0; c0 < D / 64; ++c0) {
+          const int c = tq * (D / 64) + c0;
+          uint32_t u0[32], u1[32];
+          tmem_ld32(o0 + c * 32, u0);
+          tmem_ld32(o1 + c * 32, u1);
+          tmem_wait_ld();
+          uint32_t pk[16];
 #pragma unroll
-      for (int c = 0; c < D / 32; ++c) {
-        uint32_t ov[32];
-        tmem_ld32(o_tm + c * 32, ov);
-        tmem_wait_ld();
-        uint32_t pk[16];
+          for (int i = 0; i < 16; ++i)
+            pk[i] = pack_bf16x2(__uint_as_float(u0[2 * i]) * f0 + __uint_as_float(u1[2 * i]) * f1,
+                                __uint_as_float(u0[2 * i + 1]) * f0 + __uint_as_float(u1[2 * i + 1]) * f1);
+          if (row_ok) {
+            uint4* d4 = reinterpret_cast<uint4*>(dst + c * 32);
 #pragma unroll
-        for (int i = 0; i < 16; ++i)
-          pk[i] = pack_bf16x2(__uint_as_float(ov[2 * i]) * inv_l, __uint_as_float(ov[2 * i + 1]) * inv_l);
-#ifdef CS_ATTN_DEBUG
-        if (c == 0) {
-          pk[0] = __float_as_uint(m); pk[1] = __float_as_uint(l); pk[2] = __float_as_uint(dbg_s0_keep);
-          pk[3] = __float_as_uint(dbg_s1_keep); pk[4] = dbg_mw0_keep; pk[5] = (uint32_t)nt; pk[6] = (uint32_t)U;
-          pk[7] = (uint32_t)nkeep;
+            for (int i = 0; i < 4; ++i) d4[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+          }
         }
-#endif
-        if (row_ok) {
-          uint4* d4 = reinterpret_cast<uint4*>(dst + c * 32);
+      } else {
+        const float inv_l = 1.f / l;
 #pragma unroll
-          for (int i = 0; i < 4; ++i) d4[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t ov[32];
+          tmem_ld32(o_tm + c * 32, ov);
+          tmem_wait_ld();
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            pk[i] = pack_bf16x2(__uint_as_float(ov[2 * i]) * inv_l, __uint_as_float(ov[2 * i + 1]) * inv_l);
+          if (row_ok) {
+            uint4* d4 = reinterpret_cast<uint4*>(dst + c * 32);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) d4[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+          }
         }
       }
     }
