@@ -61,21 +61,22 @@ __global__ void __launch_bounds__(256) k_init_sample(XView q, XView k, int N, in
     for (int j = threadIdx.x; j < K; j += blockDim.x) idx[j] = init[(size_t)bh * K + j];
   } else {
     for (int w = threadIdx.x; w < nwords; w += blockDim.x) sm_bits[w] = 0u;
+    // R4: splitmix64 stream, Floyd's algorithm.  The draws do not depend on the chosen set
+    // (draw i uses state seed + (i+1) * golden), so all K of them are computed in parallel:
+    // t_i = next_i % (N - K + i + 1), staged in idx[]; only the set-insertion pass is serial.
+    const long long key = (long long)(bh / X.H) * h_tot + h_off + bh % X.H;  // b*Ht + hg
+    const unsigned long long s0 = seed ^ ((unsigned long long)(key * 2 + side) * 0x9E3779B97F4A7C15ull);
+    for (int i = threadIdx.x; i < K; i += blockDim.x) {
+      unsigned long long z = s0 + (unsigned long long)(i + 1) * 0x9E3779B97F4A7C15ull;
+      z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+      z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+      z ^= z >> 31;
+      idx[i] = (int)(z % (unsigned long long)(N - K + i + 1));
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
-      // R4: splitmix64 stream, Floyd's algorithm.
-      const long long key = (long long)(bh / X.H) * h_tot + h_off + bh % X.H;  // b*Ht + hg
-      unsigned long long state = seed ^ ((unsigned long long)(key * 2 + side) * 0x9E3779B97F4A7C15ull);
-      for (int j = N - K; j < N; ++j) {
-        state += 0x9E3779B97F4A7C15ull;
-        unsigned long long z = state;
-        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-        z ^= z >> 31;
-        // z mod m = ((z_hi mod m) * 2^32 + z_lo) mod m, the second step on a value < m * 2^32
-        const unsigned m = (unsigned)(j + 1);
-        const unsigned long long hi_r = (unsigned long long)((unsigned)(z >> 32) % m);
-        const int t = (int)(((hi_r << 32) | (z & 0xffffffffull)) % m);
+      for (int i = 0; i < K; ++i) {
+        const int j = N - K + i, t = idx[i];
         const int pick = ((sm_bits[t >> 5] >> (t & 31)) & 1u) ? j : t;
         sm_bits[pick >> 5] |= 1u << (pick & 31);
       }
@@ -114,98 +115,139 @@ __global__ void __launch_bounds__(256) k_init_sample(XView q, XView k, int N, in
 }
 
 // ---------------------------------------------------------------------------------------------
-// a2: Gamma = C_a^T C_a (fp64).  grid (BH, d/8), block 256: rows e in [8 by, 8 by + 8).
-// Thread t owns column f = t % d and rows e0 + t/d + EB*i: the staged row r is read along f
-// (conflict-free) and at e (warp-uniform broadcast).
+// a2: Gamma = C_a^T C_a (fp64).  grid (BH, NB (NB+1) / 2), block 256: one 64 x 64 block of the
+// upper triangle of Gamma per CTA (an off-diagonal block also writes its mirror: Gamma is
+// symmetric); thread (ti, tj) = (t / 16, t % 16) owns the 4 x 4 outputs (e0 + 4 ti .. +3,
+// f0 + 4 tj .. +3).
+// Rows of C_a are staged in fp64 chunks of 32; per staged row 8 LDS.64 feed 16 DFMA.
 // ---------------------------------------------------------------------------------------------
 template <int D>
 __global__ void __launch_bounds__(256) k_gamma(const float* __restrict__ ca, int ka,
                                                double* __restrict__ gamma) {
-  constexpr int ROWS = 8, CH = 32, EB = 256 / D, RPT = ROWS / EB;
-  __shared__ double sa[CH][D];
-  const int bh = blockIdx.x, e0 = blockIdx.y * ROWS;
+  constexpr int CH = 32, TB = 64, NB = D / TB;
+  __shared__ __align__(16) double sa[CH][D];
+  // upper-triangle block index -> (row block, column block), column block >= row block
+  int rb = 0, cb = blockIdx.y;
+  while (cb >= NB - rb) { cb -= NB - rb; ++rb; }
+  cb += rb;
+  const int bh = blockIdx.x, e0 = rb * TB, f0 = cb * TB;
   const float* A = ca + (size_t)bh * ka * D;
-  const int t = threadIdx.x, f = t % D, eb = t / D;
-  double acc[RPT];
+  const int t = threadIdx.x, ti = t >> 4, tj = t & 15;
+  double acc[4][4];
 #pragma unroll
-  for (int i = 0; i < RPT; ++i) acc[i] = 0.0;
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
   for (int a0 = 0; a0 < ka; a0 += CH) {
     const int n = min(CH, ka - a0);
     __syncthreads();
-    for (int i = t; i < CH * D; i += 256) {
-      const int r = i / D, c = i % D;
-      sa[r][c] = r < n ? (double)A[(size_t)(a0 + r) * D + c] : 0.0;
+    for (int i = t; i < CH * D / 4; i += 256) {
+      const int r = i / (D / 4), c = (i % (D / 4)) * 4;
+      float4 v = r < n ? *reinterpret_cast<const float4*>(A + (size_t)(a0 + r) * D + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+      sa[r][c] = v.x; sa[r][c + 1] = v.y; sa[r][c + 2] = v.z; sa[r][c + 3] = v.w;
     }
     __syncthreads();
     for (int r = 0; r < n; ++r) {
-      const double vf = sa[r][f];
+      double ve[4], vf[4];
 #pragma unroll
-      for (int i = 0; i < RPT; ++i) acc[i] = fma(sa[r][e0 + eb + EB * i], vf, acc[i]);
+      for (int i = 0; i < 4; ++i) { ve[i] = sa[r][e0 + 4 * ti + i]; vf[i] = sa[r][f0 + 4 * tj + i]; }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(ve[i], vf[j], acc[i][j]);
     }
   }
+  double* G = gamma + (size_t)bh * D * D;
 #pragma unroll
-  for (int i = 0; i < RPT; ++i) gamma[(size_t)bh * D * D + (size_t)(e0 + eb + EB * i) * D + f] = acc[i];
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) G[(size_t)(e0 + 4 * ti + i) * D + f0 + 4 * tj + j] = acc[i][j];
+  if (rb != cb) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) G[(size_t)(f0 + 4 * tj + j) * D + e0 + 4 * ti + i] = acc[i][j];
+  }
 }
 
 // ---------------------------------------------------------------------------------------------
-// a2: w_j = Gamma c_j, n_j^2 = ||c_j C_a^T||^2 = c_j . w_j (Gamma = C_a^T C_a),
+// a2: w_j = Gamma c_j (= (C_s Gamma)_j, Gamma symmetric), n_j^2 = ||c_j C_a^T||^2 = c_j . w_j,
 //     W_j = w_j / n_j  ->  Wsplit[bh][j] = [bf16(W) | bf16(W - bf16(W))]
-// grid (ks_pad / 32, BH), block 256: 32 centroids per block; thread t owns output column
-// e = t % D for rows j = t / D + EB*i.  Gamma rows are read coalesced along e (Gamma is
-// symmetric).  Rows j >= ks are written as zeros (padding).
+// grid (ks_pad / 32, BH), block 256, dyn smem 2 * 32 * D doubles: 32 centroids per CTA.
+// Thread (tj, te): centroids j0 + JPT tj .. +JPT-1, output columns 4 te .. 4 te + 3 (EG = D/4
+// column groups).  Gamma is streamed through shared memory in chunks of 32 rows.  Rows j >= ks
+// are written as zeros (padding).
 // ---------------------------------------------------------------------------------------------
 template <int D>
-__global__ void __launch_bounds__(256, 1) k_anchor_w(const float* __restrict__ cs_, int ks, int ks_pad,
+__global__ void __launch_bounds__(256) k_anchor_w(const float* __restrict__ cs_, int ks, int ks_pad,
                                                   const double* __restrict__ gamma,
                                                   __nv_bfloat16* __restrict__ wsplit) {
-  constexpr int J = 32, EB = 256 / D, RPT = J / EB, WPG = D / 32;  // warps per row group
-  __shared__ double sc[J][D];
-  __shared__ double red[J][WPG];
+  constexpr int J = 32, EG = D / 4, JG = 256 / EG, JPT = J / JG, FCH = 32;
+  extern __shared__ __align__(16) double sm_aw[];
+  double (*sc)[D] = reinterpret_cast<double (*)[D]>(sm_aw);           // [J][D]   centroids
+  double (*sg)[D] = reinterpret_cast<double (*)[D]>(sm_aw + J * D);   // [FCH][D] Gamma rows
   const int bh = blockIdx.y, j0 = blockIdx.x * J, t = threadIdx.x;
-  const int e = t % D, eb = t / D;
+  const int te = t % EG, tj = t / EG;
   const float* S = cs_ + (size_t)bh * ks * D;
-  for (int i = t; i < J * D; i += 256) {
-    const int r = i / D, c = i % D;
-    sc[r][c] = (j0 + r < ks) ? (double)S[(size_t)(j0 + r) * D + c] : 0.0;
-  }
-  __syncthreads();
   const double* G = gamma + (size_t)bh * D * D;
-  double w[RPT];
-#pragma unroll
-  for (int i = 0; i < RPT; ++i) w[i] = 0.0;
-#pragma unroll 16
-  for (int f = 0; f < D; ++f) {
-    const double g = G[(size_t)f * D + e];
-#pragma unroll
-    for (int i = 0; i < RPT; ++i) w[i] = fma(g, sc[eb + EB * i][f], w[i]);
+  for (int i = t; i < J * D / 4; i += 256) {
+    const int r = i / (D / 4), c = (i % (D / 4)) * 4;
+    float4 v = (j0 + r < ks) ? *reinterpret_cast<const float4*>(S + (size_t)(j0 + r) * D + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    sc[r][c] = v.x; sc[r][c + 1] = v.y; sc[r][c + 2] = v.z; sc[r][c + 3] = v.w;
   }
-  // n_j^2 = sum_e c_j[e] w_j[e]: warp partial sums, combined in a fixed order
+  double w[JPT][4];
 #pragma unroll
-  for (int i = 0; i < RPT; ++i) {
-    double v = sc[eb + EB * i][e] * w[i];
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if ((t & 31) == 0) red[eb + EB * i][(t % D) >> 5] = v;
+  for (int i = 0; i < JPT; ++i)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) w[i][e] = 0.0;
+  for (int f0 = 0; f0 < D; f0 += FCH) {
+    __syncthreads();
+    for (int i = t; i < FCH * D / 2; i += 256) {
+      const int r = i / (D / 2), c = (i % (D / 2)) * 2;
+      const double2 g = *reinterpret_cast<const double2*>(G + (size_t)(f0 + r) * D + c);
+      sg[r][c] = g.x; sg[r][c + 1] = g.y;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int f = 0; f < FCH; ++f) {
+      double g[4], c[JPT];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) g[e] = sg[f][4 * te + e];
+#pragma unroll
+      for (int i = 0; i < JPT; ++i) c[i] = sc[JPT * tj + i][f0 + f];
+#pragma unroll
+      for (int i = 0; i < JPT; ++i)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) w[i][e] = fma(g[e], c[i], w[i][e]);
+    }
   }
-  __syncthreads();
+  // n_j^2 = sum_e c_j[e] w_j[e]: partial over this thread's 4 columns, reduced over the EG
+  // threads of the centroid group (consecutive lanes) in a fixed butterfly order
 #pragma unroll
-  for (int i = 0; i < RPT; ++i) {
-    const int jl = eb + EB * i, j = j0 + jl;
+  for (int i = 0; i < JPT; ++i) {
+    const int jl = JPT * tj + i, j = j0 + jl;
+    double n2 = 0.0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) n2 = fma(sc[jl][4 * te + e], w[i][e], n2);
+#pragma unroll
+    for (int o = EG / 2; o > 0; o >>= 1) n2 += __shfl_xor_sync(0xffffffffu, n2, o);
     if (j >= ks_pad) continue;
     __nv_bfloat16* out = wsplit + ((size_t)bh * ks_pad + j) * (2 * D);
+    __nv_bfloat16 hi[4], lo[4];
     if (j < ks) {
-      double n2 = 0.0;
-#pragma unroll
-      for (int q = 0; q < WPG; ++q) n2 += red[jl][q];
       const double inv = n2 > 0.0 ? 1.0 / sqrt(n2) : 0.0;  // ||Pbar_j|| = 0 -> W_j = 0
-      const double wv = w[i] * inv;
-      const __nv_bfloat16 hi = __double2bfloat16(wv);
-      const __nv_bfloat16 lo = __double2bfloat16(wv - (double)__bfloat162float(hi));
-      out[e] = hi;
-      out[D + e] = lo;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const double wv = w[i][e] * inv;
+        hi[e] = __double2bfloat16(wv);
+        lo[e] = __double2bfloat16(wv - (double)__bfloat162float(hi[e]));
+      }
     } else {
-      out[e] = __float2bfloat16(0.f);
-      out[D + e] = __float2bfloat16(0.f);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) { hi[e] = __float2bfloat16(0.f); lo[e] = __float2bfloat16(0.f); }
     }
+    *reinterpret_cast<uint2*>(out + 4 * te) = *reinterpret_cast<const uint2*>(hi);
+    *reinterpret_cast<uint2*>(out + D + 4 * te) = *reinterpret_cast<const uint2*>(lo);
   }
 }
 
@@ -376,11 +418,14 @@ cudaError_t launch_init_sample(XView q, XView k, int BH, int N, int d, int kq, i
 cudaError_t launch_anchor_prep(const float* ca, int ka, const float* cself, int ks, int ks_pad,
                                int BH, int d, double* gamma, __nv_bfloat16* wsplit, cudaStream_t st) {
   if (d == 128) {
-    k_gamma<128><<<dim3(BH, 128 / 8), 256, 0, st>>>(ca, ka, gamma);
-    k_anchor_w<128><<<dim3((ks_pad + 31) / 32, BH), 256, 0, st>>>(cself, ks, ks_pad, gamma, wsplit);
+    constexpr int smem = 2 * 32 * 128 * 8;
+    cudaError_t e = cudaFuncSetAttribute(k_anchor_w<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    k_gamma<128><<<dim3(BH, 3), 256, 0, st>>>(ca, ka, gamma);
+    k_anchor_w<128><<<dim3((ks_pad + 31) / 32, BH), 256, smem, st>>>(cself, ks, ks_pad, gamma, wsplit);
   } else {
-    k_gamma<64><<<dim3(BH, 64 / 8), 256, 0, st>>>(ca, ka, gamma);
-    k_anchor_w<64><<<dim3((ks_pad + 31) / 32, BH), 256, 0, st>>>(cself, ks, ks_pad, gamma, wsplit);
+    k_gamma<64><<<dim3(BH, 1), 256, 0, st>>>(ca, ka, gamma);
+    k_anchor_w<64><<<dim3((ks_pad + 31) / 32, BH), 256, 2 * 32 * 64 * 8, st>>>(cself, ks, ks_pad, gamma, wsplit);
   }
   return cudaGetLastError();
 }

@@ -15,6 +15,59 @@ __device__ __forceinline__ bool before(double va, int ia, double vb, int ib) {
   return va > vb || (va == vb && ia < ib);
 }
 
+// Block-wide bitonic sort of P2 (power of two, 256 E <= P2 <= 1024... any P2 = 256 E) entries by
+// (value desc, index asc).  Thread t holds the E consecutive entries t E .. t E + E - 1 in
+// registers: strides < E are resolved inside the thread, strides < 32 E with warp shuffles,
+// and only the strides >= 32 E (6 stages at P2 = 512) go through shared memory.
+template <int E>
+__device__ void bitonic_sort_rows(double (&v)[E], int (&ix)[E], int P2, double* sval, int* sidx) {
+  const int t = threadIdx.x;
+  for (int size = 2; size <= P2; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      if (stride < E) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          if (e & stride) continue;
+          const int e2 = e | stride;
+          const bool up = ((t * E + e) & size) == 0;
+          const bool sw = up ? before(v[e2], ix[e2], v[e], ix[e]) : before(v[e], ix[e], v[e2], ix[e2]);
+          if (sw) {
+            const double tv = v[e]; v[e] = v[e2]; v[e2] = tv;
+            const int ti = ix[e]; ix[e] = ix[e2]; ix[e2] = ti;
+          }
+        }
+      } else {
+        double vo[E];
+        int io[E];
+        if (stride < 32 * E) {
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            vo[e] = __shfl_xor_sync(0xffffffffu, v[e], stride / E);
+            io[e] = __shfl_xor_sync(0xffffffffu, ix[e], stride / E);
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < E; ++e) { sval[t * E + e] = v[e]; sidx[t * E + e] = ix[e]; }
+          __syncthreads();
+#pragma unroll
+          for (int e = 0; e < E; ++e) { vo[e] = sval[(t * E + e) ^ stride]; io[e] = sidx[(t * E + e) ^ stride]; }
+          __syncthreads();
+        }
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int i = t * E + e;
+          const bool lower = (i & stride) == 0, up = (i & size) == 0;
+          const bool take = (lower == up) ? before(vo[e], io[e], v[e], ix[e]) : before(v[e], ix[e], vo[e], io[e]);
+          if (take) { v[e] = vo[e]; ix[e] = io[e]; }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < E; ++e) { sval[t * E + e] = v[e]; sidx[t * E + e] = ix[e]; }
+  __syncthreads();
+}
+
 // Abar = C_q C_k^T in fp64.  grid (ceil(kk/32), ceil(kq/16), BH), block 256: a 16 x 32
 // output tile, each thread two dot products of length D in a fixed (sequential) order.
 template <int D>
@@ -48,7 +101,8 @@ __global__ void __launch_bounds__(256) k_abar(int kq, int kk, const float* __res
   }
 }
 
-// grid (kq, BH), block 256, dyn smem: P2 doubles + P2 ints + d doubles
+// grid (kq, BH), block 256, dyn smem: P2 doubles + P2 ints + d doubles; P2 = 256 E
+template <int E>
 __global__ void __launch_bounds__(256) k_select_rows(int kq, int kk, int d, const double* __restrict__ abar,
                                                      const int32_t* __restrict__ offs_q,
                                                      const int32_t* __restrict__ offs_k, double tau,
@@ -56,8 +110,7 @@ __global__ void __launch_bounds__(256) k_select_rows(int kq, int kk, int d, cons
   extern __shared__ double sh_d[];
   __shared__ double wred[8];
   __shared__ int first_hit;
-  int P2 = 1;
-  while (P2 < kk) P2 <<= 1;
+  constexpr int P2 = 256 * E;
   double* sval = sh_d;
   double* scq = sh_d + P2;
   int* sidx = reinterpret_cast<int*>(scq + d);
@@ -66,26 +119,17 @@ __global__ void __launch_bounds__(256) k_select_rows(int kq, int kk, int d, cons
   const int32_t* oq = offs_q + (size_t)bh * (kq + 1);
   (void)scq;
   const double* arow = abar + ((size_t)bh * kq + a) * kk;
-  for (int j = t; j < P2; j += 256) {
-    sval[j] = (j < kk && ok[j + 1] - ok[j] > 0) ? arow[j] : -INFINITY;
-    sidx[j] = j;
-  }
-  __syncthreads();
-  // bitonic sort: (value desc, index asc)
-  for (int size = 2; size <= P2; size <<= 1) {
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int i = t; i < P2; i += 256) {
-        const int jx = i ^ stride;
-        if (jx > i) {
-          const bool up = (i & size) == 0;  // "up" segments sorted by `before`
-          const double vi = sval[i], vj = sval[jx];
-          const int ii = sidx[i], ij = sidx[jx];
-          const bool swap = up ? before(vj, ij, vi, ii) : before(vi, ii, vj, ij);
-          if (swap) { sval[i] = vj; sval[jx] = vi; sidx[i] = ij; sidx[jx] = ii; }
-        }
-      }
-      __syncthreads();
+  // sort: (value desc, index asc); empty key blocks and padding are -inf
+  {
+    double v[E];
+    int ix[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int j = t * E + e;
+      v[e] = (j < kk && ok[j + 1] - ok[j] > 0) ? arow[j] : -INFINITY;
+      ix[e] = j;
     }
+    bitonic_sort_rows<E>(v, ix, P2, sval, sidx);
   }
   // number of nonempty key blocks
   int ne = 0;
@@ -107,8 +151,8 @@ __global__ void __launch_bounds__(256) k_select_rows(int kq, int kk, int d, cons
   const double sd = sqrt((double)d);
   const double mz = sval[0] / sd;
   // each thread owns 4 consecutive sorted entries (P2 <= 1024)
-  const int per = (P2 + 255) / 256;
-  double e_loc[4];
+  constexpr int per = E;
+  double e_loc[E];
   double s_loc = 0.0;
   for (int u = 0; u < per; ++u) {
     const int i = t * per + u;
@@ -256,14 +300,19 @@ cudaError_t launch_block_select(int BH, int H, int kq, int kk, int d, const floa
                                 const float* budget, double tau, double theta, int rule,
                                 int32_t* n_keep, int32_t* kept, int32_t* order, int32_t* cnt,
                                 double* abar, cudaStream_t st) {
-  int P2 = 1;
+  int P2 = 256;
   while (P2 < kk) P2 <<= 1;
   const size_t smem = (size_t)P2 * 8 + (size_t)d * 8 + (size_t)P2 * 4;
   if (d == 128)
     k_abar<128><<<dim3((kk + 31) / 32, (kq + 15) / 16, BH), 256, 0, st>>>(kq, kk, cq, ck, abar);
   else
     k_abar<64><<<dim3((kk + 31) / 32, (kq + 15) / 16, BH), 256, 0, st>>>(kq, kk, cq, ck, abar);
-  k_select_rows<<<dim3(kq, BH), 256, smem, st>>>(kq, kk, d, abar, offs_q, offs_k, tau, order, cnt);
+  if (P2 == 256)
+    k_select_rows<1><<<dim3(kq, BH), 256, smem, st>>>(kq, kk, d, abar, offs_q, offs_k, tau, order, cnt);
+  else if (P2 == 512)
+    k_select_rows<2><<<dim3(kq, BH), 256, smem, st>>>(kq, kk, d, abar, offs_q, offs_k, tau, order, cnt);
+  else
+    k_select_rows<4><<<dim3(kq, BH), 256, smem, st>>>(kq, kk, d, abar, offs_q, offs_k, tau, order, cnt);
   k_select_count<<<BH, 1024, 0, st>>>(H, kq, kk, offs_q, offs_k, cnt, budget, theta, rule, n_keep);
   k_select_emit<<<dim3(kq, BH), 256, 0, st>>>(kq, kk, order, n_keep, kept);
   return cudaGetLastError();

@@ -255,6 +255,44 @@ def test_attn_tiny_clusters_and_single_query_cluster(pb):
     assert err.max() <= ATOL_MAX and err.mean() <= ATOL_MEAN
 
 
+@pytest.mark.parametrize("d", [64, 128])
+def test_attn_split_kv_single_tile_items(pb, d):
+    """Work items with one query tile run split-KV (even / odd KV tiles on the two accumulator
+    sets, merged in the epilogue).  Query clusters of 1..4 tiles (single, pair, pair + single)
+    against kept key sets of 1..9 KV tiles (odd and even counts, one tile only)."""
+    rng = np.random.default_rng(5)
+    q_sizes = [60, 128, 129, 300, 1, 500, 77, 255]
+    k_sizes = [3, 5, 130, 64, 200, 1, 90, 257, 40, 128, 33, 400, 8, 16, 300, 7]
+    N = max(sum(q_sizes), sum(k_sizes))
+    q_sizes[-1] += N - sum(q_sizes)
+    k_sizes[-1] += N - sum(k_sizes)
+    kq, kk = len(q_sizes), len(k_sizes)
+    Lq = rng.permutation(np.repeat(np.arange(kq), q_sizes))
+    Lk = rng.permutation(np.repeat(np.arange(kk), k_sizes))
+    w = random_qkv(1, 1, N, d, seed=31)
+    pq, oq = svoo.counting_sort(Lq, kq)
+    pk, ok = svoo.counting_sort(Lk, kk)
+    n_keep = 4
+    kept = np.full((kq, kk), -1, np.int64)
+    sel = []
+    for a in range(kq):
+        if a == 0:
+            ka = np.array([0, 1, 5, 12])                 # 17 keys -> a single KV tile
+        elif a == 1:
+            ka = np.array([0, 2, 5, 12])                 # 144 keys -> two KV tiles
+        else:
+            ka = np.sort(rng.choice(kk, n_keep, replace=False))
+        kept[a, :n_keep] = ka
+        sel.append(ka)
+    t = lambda x: torch.from_numpy(x.astype(np.int32))[None, None].cuda()
+    O = pb.block_sparse_attn(w.q.cuda(), w.k.cuda(), w.v.cuda(), t(pq), t(oq), t(pk), t(ok),
+                             torch.tensor([[n_keep]], dtype=torch.int32).cuda(),
+                             torch.from_numpy(kept.astype(np.int32))[None, None].cuda())
+    ref = svoo.sparse_attention(f64(w.q[0, 0]), f64(w.k[0, 0]), f64(w.v[0, 0]), Lq, Lk, sel)
+    err = np.abs(f64(O[0, 0]) - ref)
+    assert err.max() <= ATOL_MAX and err.mean() <= ATOL_MEAN, (err.max(), err.mean())
+
+
 def test_attn_singleton_keys_pick_value(pb):
     """singleton key blocks, one kept block per query block -> o_i = v_{j*}."""
     d, N = 128, 256
