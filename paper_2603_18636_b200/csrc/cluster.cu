@@ -117,8 +117,9 @@ __global__ void __launch_bounds__(256) k_init_sample(XView q, XView k, int N, in
 // ---------------------------------------------------------------------------------------------
 // a2: Gamma = C_a^T C_a (fp64).  grid (BH, NB (NB+1) / 2), block 256: one 64 x 64 block of the
 // upper triangle of Gamma per CTA (an off-diagonal block also writes its mirror: Gamma is
-// symmetric); thread (ti, tj) = (t / 16, t % 16) owns the 4 x 4 outputs (e0 + 4 ti .. +3,
-// f0 + 4 tj .. +3).
+// symmetric); thread (ti, tj) = (t / 16, t % 16) owns the 4 x 4 outputs (e0 + ti + 16 i,
+// f0 + tj + 16 j): the 16 lanes of a half-warp read 16 consecutive doubles (one wavefront) and
+// the two halves the same ones (broadcast).
 // Rows of C_a are staged in fp64 chunks of 32; per staged row 8 LDS.64 feed 16 DFMA.
 // ---------------------------------------------------------------------------------------------
 template <int D>
@@ -150,7 +151,7 @@ __global__ void __launch_bounds__(256) k_gamma(const float* __restrict__ ca, int
     for (int r = 0; r < n; ++r) {
       double ve[4], vf[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) { ve[i] = sa[r][e0 + 4 * ti + i]; vf[i] = sa[r][f0 + 4 * tj + i]; }
+      for (int i = 0; i < 4; ++i) { ve[i] = sa[r][e0 + ti + 16 * i]; vf[i] = sa[r][f0 + tj + 16 * i]; }
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -161,12 +162,12 @@ __global__ void __launch_bounds__(256) k_gamma(const float* __restrict__ ca, int
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) G[(size_t)(e0 + 4 * ti + i) * D + f0 + 4 * tj + j] = acc[i][j];
+    for (int j = 0; j < 4; ++j) G[(size_t)(e0 + ti + 16 * i) * D + f0 + tj + 16 * j] = acc[i][j];
   if (rb != cb) {
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) G[(size_t)(f0 + 4 * tj + j) * D + e0 + 4 * ti + i] = acc[i][j];
+      for (int j = 0; j < 4; ++j) G[(size_t)(f0 + tj + 16 * j) * D + e0 + ti + 16 * i] = acc[i][j];
   }
 }
 
@@ -174,8 +175,8 @@ __global__ void __launch_bounds__(256) k_gamma(const float* __restrict__ ca, int
 // a2: w_j = Gamma c_j (= (C_s Gamma)_j, Gamma symmetric), n_j^2 = ||c_j C_a^T||^2 = c_j . w_j,
 //     W_j = w_j / n_j  ->  Wsplit[bh][j] = [bf16(W) | bf16(W - bf16(W))]
 // grid (ks_pad / 32, BH), block 256, dyn smem 2 * 32 * D doubles: 32 centroids per CTA.
-// Thread (tj, te): centroids j0 + JPT tj .. +JPT-1, output columns 4 te .. 4 te + 3 (EG = D/4
-// column groups).  Gamma is streamed through shared memory in chunks of 32 rows.  Rows j >= ks
+// Thread (tj, te): centroids j0 + JPT tj .. +JPT-1, output columns te + EG e, e < 4 (EG = D/4;
+// consecutive lanes read consecutive Gamma columns).  Gamma is streamed through shared memory in chunks of 32 rows.  Rows j >= ks
 // are written as zeros (padding).
 // ---------------------------------------------------------------------------------------------
 template <int D>
@@ -212,7 +213,7 @@ __global__ void __launch_bounds__(256) k_anchor_w(const float* __restrict__ cs_,
     for (int f = 0; f < FCH; ++f) {
       double g[4], c[JPT];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) g[e] = sg[f][4 * te + e];
+      for (int e = 0; e < 4; ++e) g[e] = sg[f][te + EG * e];
 #pragma unroll
       for (int i = 0; i < JPT; ++i) c[i] = sc[JPT * tj + i][f0 + f];
 #pragma unroll
@@ -228,7 +229,7 @@ __global__ void __launch_bounds__(256) k_anchor_w(const float* __restrict__ cs_,
     const int jl = JPT * tj + i, j = j0 + jl;
     double n2 = 0.0;
 #pragma unroll
-    for (int e = 0; e < 4; ++e) n2 = fma(sc[jl][4 * te + e], w[i][e], n2);
+    for (int e = 0; e < 4; ++e) n2 = fma(sc[jl][te + EG * e], w[i][e], n2);
 #pragma unroll
     for (int o = EG / 2; o > 0; o >>= 1) n2 += __shfl_xor_sync(0xffffffffu, n2, o);
     if (j >= ks_pad) continue;
@@ -246,17 +247,19 @@ __global__ void __launch_bounds__(256) k_anchor_w(const float* __restrict__ cs_,
 #pragma unroll
       for (int e = 0; e < 4; ++e) { hi[e] = __float2bfloat16(0.f); lo[e] = __float2bfloat16(0.f); }
     }
-    *reinterpret_cast<uint2*>(out + 4 * te) = *reinterpret_cast<const uint2*>(hi);
-    *reinterpret_cast<uint2*>(out + D + 4 * te) = *reinterpret_cast<const uint2*>(lo);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) { out[te + EG * e] = hi[e]; out[D + te + EG * e] = lo[e]; }
   }
 }
 
 // ---------------------------------------------------------------------------------------------
-// a5/a7: centroid update.  grid (K, BH), block 256 (8 warps); warp w sums a contiguous chunk of
-// the cluster's sorted positions; fixed order -> deterministic.  Empty cluster: untouched (R5).
+// a5/a7: centroid update.  grid (ceil(K / CPB), BH), block 256 (8 warps), CPB = 8 / NWC clusters
+// per CTA with NWC warps each (NWC from the mean cluster size, so small clusters do not leave
+// most of a CTA idle).  Warp ws of a cluster sums a contiguous chunk of its sorted positions;
+// fixed order -> deterministic.  Empty cluster: untouched (R5).
 // ---------------------------------------------------------------------------------------------
 template <int D>
-__global__ void __launch_bounds__(256) k_seg_mean(XView x, int N, int K,
+__global__ void __launch_bounds__(256) k_seg_mean(XView x, int N, int K, int nwc,
                                                   const int32_t* __restrict__ perm,
                                                   const int32_t* __restrict__ offs,
                                                   float* __restrict__ C,
@@ -265,17 +268,18 @@ __global__ void __launch_bounds__(256) k_seg_mean(XView x, int N, int K,
   constexpr int RPW = 32 / LPR;     // rows per warp instruction (2 or 4)
   constexpr int NW = 8, U = 8;      // warps, rows in flight per lane group
   __shared__ float part[NW * RPW][D];
-  const int bh = blockIdx.y, j = blockIdx.x;
+  const int bh = blockIdx.y;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int cpb = NW / nwc, cl = w / nwc, ws = w % nwc;
+  const int j = blockIdx.x * cpb + cl;
   const int grp = lane / LPR, gl = lane % LPR;  // row group inside the warp, lane inside the row
   const int32_t* of = offs + (size_t)bh * (K + 1);
-  const int beg = of[j], end = of[j + 1], cnt = end - beg;
-  if (cnt == 0) return;
+  const int beg = j < K ? of[j] : 0, end = j < K ? of[j + 1] : 0, cnt = end - beg;
   const int b = bh / x.H, h = bh % x.H;
-  // fixed partition of the cluster's positions: warp w owns a contiguous chunk, row group grp
+  // fixed partition of the cluster's positions: warp ws owns a contiguous chunk, row group grp
   // takes every RPW-th position of it -> deterministic summation order
-  const int chunk = (cnt + NW - 1) / NW;
-  const int p0 = beg + w * chunk, p1 = min(end, p0 + chunk);
+  const int chunk = (cnt + nwc - 1) / nwc;
+  const int p0 = beg + ws * chunk, p1 = min(end, p0 + chunk);
   const int32_t* pm = perm + (size_t)bh * N;
   float acc[8];
 #pragma unroll
@@ -300,11 +304,15 @@ __global__ void __launch_bounds__(256) k_seg_mean(XView x, int N, int K,
 #pragma unroll
   for (int i = 0; i < 8; ++i) part[w * RPW + grp][gl * 8 + i] = acc[i];
   __syncthreads();
-  if (threadIdx.x < D) {
-    float s = 0.f;
-#pragma unroll
-    for (int q = 0; q < NW * RPW; ++q) s += part[q][threadIdx.x];
-    C[((size_t)bh * K + j) * D + threadIdx.x] = s / (float)cnt;
+  // cluster c of the CTA: partial rows [c nwc RPW, (c+1) nwc RPW), summed in a fixed order
+  for (int o = threadIdx.x; o < cpb * D; o += 256) {
+    const int c = o / D, col = o % D, jc = blockIdx.x * cpb + c;
+    if (jc >= K) continue;
+    const int n = of[jc + 1] - of[jc];
+    if (n == 0) continue;
+    float sum = 0.f;
+    for (int q = 0; q < nwc * RPW; ++q) sum += part[c * nwc * RPW + q][col];
+    C[((size_t)bh * K + jc) * D + col] = sum / (float)n;
   }
 }
 
@@ -432,10 +440,15 @@ cudaError_t launch_anchor_prep(const float* ca, int ka, const float* cself, int 
 
 cudaError_t launch_seg_mean(XView x, int BH, int N, int d, int K, const int32_t* perm,
                             const int32_t* offs, float* C, __nv_bfloat16* xperm, cudaStream_t st) {
+  // warps per cluster: about one warp per 64 mean members, a power of two in [1, 8]
+  const int mean = N / K;
+  int nwc = 1;
+  while (nwc < 8 && nwc * 64 < mean) nwc <<= 1;
+  const dim3 grid((K + 8 / nwc - 1) / (8 / nwc), BH);
   if (d == 128)
-    k_seg_mean<128><<<dim3(K, BH), 256, 0, st>>>(x, N, K, perm, offs, C, xperm);
+    k_seg_mean<128><<<grid, 256, 0, st>>>(x, N, K, nwc, perm, offs, C, xperm);
   else
-    k_seg_mean<64><<<dim3(K, BH), 256, 0, st>>>(x, N, K, perm, offs, C, xperm);
+    k_seg_mean<64><<<grid, 256, 0, st>>>(x, N, K, nwc, perm, offs, C, xperm);
   return cudaGetLastError();
 }
 
