@@ -22,7 +22,10 @@ Functions and their pins (tests/test_oracle_*.py):
                                                           "parity unpinned" end to end: the paper
                                                           prints no worked example.
   counting_sort                             implied P:1266 pinned: np.argsort(kind="stable")
-  select_blocks (Ā, Recall, ρ rule, top-ρK)  P:1247-1257   pinned: SPEC worked examples, nesting
+  select_blocks (Ā, Recall, ρ rule, top-ρK)  P:1247-1257   pinned: SPEC worked examples, nesting;
+    + NEXT-4 variants (per_row, size_weighted)            pinned: reduce to the base reading
+                                                          (FIXED / equal sizes), closed-form
+                                                          size-weighted masses, hand example
   sparse_attention                          P:1257        pinned: ρ=1 == library SDPA, singleton
                                                           case, n=8 brute force, convexity
 """
@@ -262,16 +265,19 @@ def rule_count(n_rec: int, budget: float, theta: float, rule: int, Kk: int, Kk_n
 @dataclass
 class SelectResult:
     n_keep: int
-    kept: np.ndarray        # [K_q, n_keep] ascending key-block indices
+    kept: object            # [K_q, n_keep] ascending key-block indices (a list of per-row arrays
+                            # when per_row: row a has n_rows[a] entries)
     c: np.ndarray           # per query block: minimal #key blocks covering tau (0 for empty rows)
     n_rec: int
     n_bud: int
     Abar: np.ndarray
+    n_rows: np.ndarray | None = None  # per-row counts (per_row only)
 
 
 def select_blocks(Cq: np.ndarray, Ck: np.ndarray, sizes_q: np.ndarray, sizes_k: np.ndarray,
                   budget: float, tau: float, theta: float, rule: int,
-                  d_head: int | None = None) -> SelectResult:
+                  d_head: int | None = None, per_row: bool = False,
+                  size_weighted: bool = False) -> SelectResult:
     """Coarse estimate, Recall, the threshold rule and top-rho K_k selection for one head.
 
     Abar = C_q C_k^T
@@ -285,6 +291,14 @@ def select_blocks(Cq: np.ndarray, Ck: np.ndarray, sizes_q: np.ndarray, sizes_k: 
         FIXED      : n = n_b
     clamp n to [1, K_k'] ; kept[a] = the n key blocks with largest raw Abar_a (ties -> lowest
     index, empty key blocks never eligible), listed ascending (R11: same n every row).
+
+    Variants of the readings R9 / R11 (R9c / R11b):
+      size_weighted : block importance z_ac = Abar_ac / sqrt(d) + log|K_c| (the softmax mass of a
+                      key block = the total attention mass its |K_c| tokens would get if each
+                      had the centroid logit); ranking and Recall both use z (desc, index asc).
+      per_row       : each nonempty query block a keeps n_a = rule(c_a) blocks — the same rho rule
+                      with its own recall count c_a in place of the row mean n_rec; empty query
+                      blocks keep the shared n.
     """
     Cq = np.asarray(Cq, np.float64)
     Ck = np.asarray(Ck, np.float64)
@@ -299,16 +313,28 @@ def select_blocks(Cq: np.ndarray, Ck: np.ndarray, sizes_q: np.ndarray, sizes_k: 
     cand = np.nonzero(ne_k)[0]
     orders = []
     c = np.zeros(Kq, dtype=np.int64)
+    logsize = np.log(np.asarray(sizes_k, np.float64)[cand]) if size_weighted else None
     for a in range(Kq):
-        vals = A[a, cand]
-        # descending raw Abar, ties -> lower index (stable sort on the negated values)
-        o = cand[np.argsort(-vals, kind="stable")]
+        if size_weighted:
+            z = A[a, cand] / math.sqrt(d_head) + logsize
+            o = cand[np.argsort(-z, kind="stable")]          # descending z, ties -> lower index
+            zs = z[np.argsort(-z, kind="stable")]
+        else:
+            vals = A[a, cand]
+            # descending raw Abar, ties -> lower index (stable sort on the negated values)
+            o = cand[np.argsort(-vals, kind="stable")]
+            zs = A[a, o] / math.sqrt(d_head)
         orders.append(o)
         if ne_q[a]:
-            c[a] = recall_count(softmax_row(A[a, o] / math.sqrt(d_head)), float(tau))
+            c[a] = recall_count(softmax_row(zs), float(tau))
     n_rec = (int(c.sum()) + Kq_ne - 1) // Kq_ne
     n_b = n_from_ratio(float(np.float32(budget)), Kk)
     n = rule_count(n_rec, budget, theta, rule, Kk, Kk_ne)
+    if per_row:
+        n_rows = np.array([rule_count(int(c[a]), budget, theta, rule, Kk, Kk_ne) if ne_q[a] else n
+                           for a in range(Kq)], dtype=np.int64)
+        kept = [np.sort(orders[a][:n_rows[a]]).astype(np.int64) for a in range(Kq)]
+        return SelectResult(n, kept, c, n_rec, n_b, A, n_rows)
     kept = np.stack([np.sort(o[:n]) for o in orders]).astype(np.int64)
     return SelectResult(n, kept, c, n_rec, n_b, A)
 

@@ -342,3 +342,79 @@ def test_toy_config_runs_fast():
     assert time.time() - t0 < 30
     assert r.sel.n_keep >= 1 and r.O.shape == (2048, 64)
     assert np.isfinite(r.O).all()
+
+
+# ------------------------------------------------------------------ NEXT-4 selection variants
+def _rand_select_inputs(seed, kq=12, kk=30, d=16):
+    rng = np.random.default_rng(seed)
+    Cq, Ck = rng.normal(size=(kq, d)), rng.normal(size=(kk, d))
+    sq = rng.integers(0, 9, kq)
+    sk = rng.integers(0, 9, kk)
+    sq[0] = sk[0] = 3  # at least one nonempty block on each side
+    return Cq, Ck, sq, sk
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_size_weighted_equal_sizes_reduces_to_base(seed):
+    """log|K_c| is a constant when all key blocks have the same size: softmax and ranking are
+    shift invariant, so the weighted selection equals the base reading (R9)."""
+    Cq, Ck, sq, _ = _rand_select_inputs(seed)
+    sk = np.full(Ck.shape[0], 5)
+    for rule in (svoo.RULE_DENSITY, svoo.RULE_FIXED):
+        a = svoo.select_blocks(Cq, Ck, sq, sk, 0.2, 0.9, 0.1, rule)
+        b = svoo.select_blocks(Cq, Ck, sq, sk, 0.2, 0.9, 0.1, rule, size_weighted=True)
+        assert a.n_keep == b.n_keep and np.array_equal(a.c, b.c)
+        assert np.array_equal(a.kept, b.kept)
+
+
+def test_size_weighted_closed_form_masses():
+    """Two key blocks with the same centroid logit but sizes 1 and 9: the weighted masses are
+    1/10 and 9/10 (p_c = |K_c| e^{z_c} / sum |K| e^z), so tau = 0.85 is covered by the large
+    block alone (c = 1) while the unweighted masses 1/2, 1/2 need both (c = 2)."""
+    Cq = np.array([[1.0, 0.0]])
+    Ck = np.array([[1.0, 0.0], [1.0, 0.0], [-50.0, 0.0]])
+    sq, sk = np.array([4]), np.array([1, 9, 2])
+    w = svoo.select_blocks(Cq, Ck, sq, sk, 1.0, 0.85, 0.1, svoo.RULE_FIXED, size_weighted=True)
+    u = svoo.select_blocks(Cq, Ck, sq, sk, 1.0, 0.85, 0.1, svoo.RULE_FIXED)
+    assert w.c[0] == 1 and u.c[0] == 2
+    # the weighted order puts block 1 (size 9) first; the unweighted tie goes to index 0
+    p_w = np.array([1.0, 9.0]) / 10.0
+    assert p_w[1] >= 0.85 > p_w[0]
+    z = Cq @ Ck.T / math.sqrt(2) + np.log(sk)
+    assert np.argmax(z[0]) == 1
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_per_row_fixed_equals_shared(seed):
+    """FIXED: every row keeps n_b blocks, so per-row counts equal the shared count."""
+    Cq, Ck, sq, sk = _rand_select_inputs(seed)
+    a = svoo.select_blocks(Cq, Ck, sq, sk, 0.3, 0.9, 0.1, svoo.RULE_FIXED)
+    b = svoo.select_blocks(Cq, Ck, sq, sk, 0.3, 0.9, 0.1, svoo.RULE_FIXED, per_row=True)
+    assert np.all(b.n_rows == a.n_keep)
+    assert all(np.array_equal(a.kept[r], b.kept[r]) for r in range(len(sq)))
+
+
+def test_per_row_hand_example():
+    """Row 0 has one dominant key block (c_0 = 1), row 1 three equal ones (masses 1/3 each,
+    tau = 0.9 -> c_1 = 3).  Budget 0.5 of 6 blocks -> n_b = 3, density rule with 1-b > theta ->
+    min.  Shared (R11): n_rec = ceil(4/2) = 2 -> both rows keep 2.  Per row: 1 and 3."""
+    Cq = np.array([[20.0, 0.0], [0.0, 20.0]])
+    Ck = np.array([[20.0, 0.0], [0.0, 20.0], [0.0, 20.0], [0.0, 20.0], [0.0, 0.0], [0.0, 0.0]])
+    sq, sk = np.array([5, 5]), np.ones(6, int)
+    sh = svoo.select_blocks(Cq, Ck, sq, sk, 0.5, 0.9, 0.1, svoo.RULE_DENSITY)
+    pr = svoo.select_blocks(Cq, Ck, sq, sk, 0.5, 0.9, 0.1, svoo.RULE_DENSITY, per_row=True)
+    assert list(sh.c) == [1, 3] and sh.n_rec == 2 and sh.n_keep == 2
+    assert sh.kept.tolist() == [[0, 1], [1, 2]]
+    assert pr.n_rows.tolist() == [1, 3]
+    assert [k.tolist() for k in pr.kept] == [[0], [1, 2, 3]]
+
+
+def test_per_row_empty_query_block_keeps_shared_n():
+    Cq, Ck, sq, sk = _rand_select_inputs(7)
+    sq[3] = 0
+    pr = svoo.select_blocks(Cq, Ck, sq, sk, 0.2, 0.9, 0.1, svoo.RULE_DENSITY, per_row=True)
+    assert pr.n_rows[3] == pr.n_keep
+    for a in range(len(sq)):
+        if sq[a] > 0:
+            assert pr.n_rows[a] == svoo.rule_count(int(pr.c[a]), 0.2, 0.1, svoo.RULE_DENSITY, len(sk),
+                                                   int((sk > 0).sum()))
