@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--reuse-steps", type=int, default=1,
                     help="also time the clustering-reuse step (P:1261-1262) and report amortised ms")
+    ap.add_argument("--sel-flags", type=int, default=0,
+                    help="selection variants (NEXT-4): 1 = per-row counts (R11b), 2 = size-weighted (R9c)")
     ap.add_argument("--parallel", choices=["head", "ulysses"], default=None,
                     help="multi-GPU split (default: ulysses for hunyuan_720p, head-parallel otherwise)")
     ap.add_argument("--cpu-sample-rows", type=int, default=1500,
@@ -223,7 +225,7 @@ def run_ours(args):
         out = torch.empty_like(q)
         budget = budget_all[h0:h1].contiguous()
         kw = dict(seed=args.seed, tau=args.tau, theta=args.theta, rule=rule, out=out, ws=ws, head_offset=h0,
-                  heads_total=H_total)
+                  heads_total=H_total, sel_flags=args.sel_flags)
 
         def step(evs=None, qq=None, kk_=None, vv=None):
             return pb.coclust_sparse_attention(q if qq is None else qq, k if kk_ is None else kk_,
@@ -238,19 +240,22 @@ def run_ours(args):
     # same bits as inside the fused call)
     st = pb.coclust_assign(q_h, k_h, args.kq, args.kk, args.iters, seed=args.seed, ws=ws, head_offset=h0,
                            heads_total=H_total)
-    n_keep, kept = pb.block_select(st["cq"], st["ck"], st["offs_q"], st["offs_k"],
-                                   budget_all[h0:h1].contiguous(), args.tau, args.theta, rule, ws=ws)
+    sel = pb.block_select(st["cq"], st["ck"], st["offs_q"], st["offs_k"], budget_all[h0:h1].contiguous(),
+                          args.tau, args.theta, rule, ws=ws, flags=args.sel_flags if mode == "head" else 0)
+    n_keep, kept = sel[0], sel[1]
     torch.cuda.synchronize()
     oq = st["offs_q"].cpu().numpy().reshape(B * H, -1)
     ok = st["offs_k"].cpu().numpy().reshape(B * H, -1)
     kp = kept.cpu().numpy().reshape(B * H, args.kq, args.kk)
     nk = n_keep.cpu().numpy().reshape(-1)
+    nrows = (sel[2].cpu().numpy().reshape(B * H, args.kq) if len(sel) > 2
+             else np.repeat(nk[:, None], args.kq, 1))
     f_kept = 0
     for bh in range(B * H):
         sq, sk = np.diff(oq[bh]), np.diff(ok[bh])
-        f_kept += int((sq * sk[kp[bh, :, :nk[bh]]].sum(1)).sum())
+        f_kept += int(sum(int(sq[a]) * int(sk[kp[bh, a, :nrows[bh, a]]].sum()) for a in range(args.kq)))
     f_kept *= 4 * d
-    del st, n_keep, kept, q_h, k_h
+    del st, sel, n_keep, kept, q_h, k_h
 
     for _ in range(max(args.warmup, 1)):
         step()
@@ -384,7 +389,7 @@ def run_ours(args):
         "dense_equiv_tflops": dense_flops / (ms * 1e-3) / 1e12,
         "config": {"workload": CONFIG_NAMES[args.config], "B": B, "H": H_total, "N": N, "d": d,
                    "kq": args.kq, "kk": args.kk, "iters": args.iters, "budget": args.budget,
-                   "rule": args.rule, "tau": args.tau, "theta": args.theta,
+                   "rule": args.rule, "tau": args.tau, "theta": args.theta, "sel_flags": args.sel_flags,
                    "parallelism": (f"ulysses-a2a x{world}" if mode == "ulysses" else f"head-parallel x{world}"),
                    "l2": "inputs larger than L2 (%.0f MB/tensor/rank)" % (q.numel() * 2 / 1e6)},
         "kept_tflop_per_layer": f_kept_total / 1e12,

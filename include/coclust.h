@@ -126,6 +126,28 @@ cs_status block_select(int B, int H, int kq, int kk, int d, const float* cq, con
                        double tau, double theta, int rule, int32_t* n_keep, int32_t* kept,
                        void* ws, size_t ws_bytes, void* stream);
 
+/* Selection variants (the paper's Recall and "top rho K_k" are open to these
+ * readings, R9c / R11b).  Bit flags: */
+enum {
+  /* R11b: each nonempty query block a keeps n_a = rule(c_a) blocks (the same rho rule with its
+   * own recall count in place of the row mean n_rec); empty query blocks keep the shared n. */
+  CS_SEL_PER_ROW = 1,
+  /* R9c: block importance z_ac = Abar_ac / sqrt(d) + log|K_c| (softmax mass of a key block =
+   * the mass its |K_c| tokens would get at the centroid logit); ranking and Recall both use z
+   * (descending, ties -> lower index). */
+  CS_SEL_SIZE_WEIGHTED = 2
+};
+
+/* block_select with selection flags.  n_keep [B,H] always receives the shared count (R11);
+ * n_keep_rows [B,H,kq] (required with CS_SEL_PER_ROW, else nullable) receives the per-row counts
+ * (the shared n in every row without CS_SEL_PER_ROW); kept row a holds n_keep_rows[a] ascending
+ * entries.  Unknown flag bits -> CS_ERR_ARG. */
+cs_status block_select_ex(int B, int H, int kq, int kk, int d, const float* cq, const float* ck,
+                          const int32_t* offs_q, const int32_t* offs_k, const float* budget,
+                          double tau, double theta, int rule, int flags, int32_t* n_keep,
+                          int32_t* n_keep_rows, int32_t* kept, void* ws, size_t ws_bytes,
+                          void* stream);
+
 /* Block-sparse attention over the kept blocks:
  *   for query i in cluster a: o_i = sum_{j: L_k(j) in kept[a]} softmax_j(q_i.k_j * scale) v_j,
  * written in ORIGINAL token order (the inverse permutation is fused into the stores).  bf16 MMA,
@@ -135,6 +157,14 @@ cs_status block_sparse_attn(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in
                             const int32_t* perm_k, const int32_t* offs_k, const int32_t* n_keep,
                             const int32_t* kept, float scale, cs_bf16_out o, void* ws,
                             size_t ws_bytes, void* stream);
+
+/* block_sparse_attn with per-row kept counts: n_keep_rows [B,H,kq] (nullable -> n_keep[b,h] for
+ * every row), as written by block_select_ex. */
+cs_status block_sparse_attn_ex(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in k, cs_bf16_in v,
+                               int kq, int kk, const int32_t* perm_q, const int32_t* offs_q,
+                               const int32_t* perm_k, const int32_t* offs_k, const int32_t* n_keep,
+                               const int32_t* n_keep_rows, const int32_t* kept, float scale,
+                               cs_bf16_out o, void* ws, size_t ws_bytes, void* stream);
 
 /* The whole layer: coclust_assign -> block_select -> block_sparse_attn, on device only (no host
  * round trip; CUDA-graph capturable).  budget [H] is indexed by the local head h; head_offset /
@@ -147,6 +177,14 @@ cs_status coclust_sparse_attention(int B, int H, int N, int d, cs_bf16_in q, cs_
                                    const float* budget, double tau, double theta, int rule,
                                    float scale, cs_bf16_out o, void* ws, size_t ws_bytes,
                                    void* stream, void* const* stage_events);
+
+/* coclust_sparse_attention with selection flags (CS_SEL_*); sel_flags = 0 is the base entry. */
+cs_status coclust_sparse_attention_ex(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in k,
+                                      cs_bf16_in v, int kq, int kk, int iters, uint64_t seed,
+                                      int head_offset, int heads_total, const float* budget,
+                                      double tau, double theta, int rule, int sel_flags,
+                                      float scale, cs_bf16_out o, void* ws, size_t ws_bytes,
+                                      void* stream, void* const* stage_events);
 
 /* Clustering-reuse state ("we reuse the clustering results and recompute them every
  * N steps").  Caller-owned device buffers, shapes as in coclust_assign /
@@ -162,6 +200,7 @@ typedef struct {
   int32_t* offs_k; /* [B,H,kk+1] */
   int32_t* n_keep; /* [B,H]      */
   int32_t* kept;   /* [B,H,kq,kk]*/
+  int32_t* n_keep_rows; /* [B,H,kq] per-row counts; NULL allowed unless sel_flags has CS_SEL_PER_ROW */
 } cs_layer_state;
 
 /* coclust_sparse_attention with caller-owned state: recompute != 0 runs co-clustering and selection
@@ -170,8 +209,9 @@ typedef struct {
 cs_status coclust_sparse_attention_cached(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in k,
                                           cs_bf16_in v, int kq, int kk, int iters, uint64_t seed,
                                           int head_offset, int heads_total, const float* budget,
-                                          double tau, double theta, int rule, float scale,
-                                          cs_bf16_out o, const cs_layer_state* state, int recompute,
+                                          double tau, double theta, int rule, int sel_flags,
+                                          float scale, cs_bf16_out o, const cs_layer_state* state,
+                                          int recompute,
                                           void* ws, size_t ws_bytes, void* stream,
                                           void* const* stage_events);
 

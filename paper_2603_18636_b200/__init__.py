@@ -19,6 +19,7 @@ __all__ = [
 ]
 
 RULE_DENSITY, RULE_AS_WRITTEN, RULE_FIXED = 0, 1, 2
+SEL_PER_ROW, SEL_SIZE_WEIGHTED = 1, 2  # block_select_ex flags (include/coclust.h, NEXT-4)
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("COCLUST_LIB", os.path.join(_HERE, "libcoclust.so"))
 
@@ -59,11 +60,18 @@ _SIG = {
     "coclust_sparse_attention": (_I, [_I, _I, _I, _I, _BF16In, _BF16In, _BF16In, _I, _I, _I,
                                       ctypes.c_uint64, _I, _I, _P, ctypes.c_double, ctypes.c_double, _I,
                                       ctypes.c_float, _BF16Out, _P, ctypes.c_size_t, _P, _P]),
+    "block_select_ex": (_I, [_I, _I, _I, _I, _I, _P, _P, _P, _P, _P, ctypes.c_double, ctypes.c_double,
+                             _I, _I, _P, _P, _P, _P, ctypes.c_size_t, _P]),
+    "block_sparse_attn_ex": (_I, [_I, _I, _I, _I, _BF16In, _BF16In, _BF16In, _I, _I, _P, _P, _P, _P, _P,
+                                  _P, _P, ctypes.c_float, _BF16Out, _P, ctypes.c_size_t, _P]),
+    "coclust_sparse_attention_ex": (_I, [_I, _I, _I, _I, _BF16In, _BF16In, _BF16In, _I, _I, _I,
+                                         ctypes.c_uint64, _I, _I, _P, ctypes.c_double, ctypes.c_double, _I,
+                                         _I, ctypes.c_float, _BF16Out, _P, ctypes.c_size_t, _P, _P]),
     "cs_block_transpose": (_I, [_I, _I, ctypes.c_size_t, _P, _P, _P]),
     "coclust_sparse_attention_cached": (_I, [_I, _I, _I, _I, _BF16In, _BF16In, _BF16In, _I, _I, _I,
                                              ctypes.c_uint64, _I, _I, _P, ctypes.c_double, ctypes.c_double,
-                                             _I, ctypes.c_float, _BF16Out, _P, _I, _P, ctypes.c_size_t, _P,
-                                             _P]),
+                                             _I, _I, ctypes.c_float, _BF16Out, _P, _I, _P, ctypes.c_size_t,
+                                             _P, _P]),
 }
 
 _lib = None
@@ -196,14 +204,24 @@ def coclust_permute(labels, k, ws=None):
     return perm, offs
 
 
-def block_select(cq, ck, offs_q, offs_k, budget, tau=0.95, theta=0.1, rule=RULE_DENSITY, ws=None):
-    """-> (n_keep [B,H] int32, kept [B,H,kq,kk] int32; first n_keep entries per row valid)."""
+def block_select(cq, ck, offs_q, offs_k, budget, tau=0.95, theta=0.1, rule=RULE_DENSITY, ws=None,
+                 flags=0):
+    """-> (n_keep [B,H] int32, kept [B,H,kq,kk] int32; first n_keep entries per row valid).
+    flags (SEL_PER_ROW | SEL_SIZE_WEIGHTED, NEXT-4) != 0 -> block_select_ex, and the result gets a
+    third element n_keep_rows [B,H,kq] (row a of kept holds n_keep_rows[a] entries)."""
     _cuda(cq, "cq")
     B, H, kq, d = cq.shape
     kk = ck.shape[2]
     n_keep = torch.empty(B, H, dtype=torch.int32, device=cq.device)
     kept = torch.full((B, H, kq, kk), -1, dtype=torch.int32, device=cq.device)
     w, wn = _ws(ws, B * H * kq * (kk + 1) * 4 + B * H * kq * kk * 8 + 4096, cq.device)
+    if flags:
+        n_rows = torch.empty(B, H, kq, dtype=torch.int32, device=cq.device)
+        _check(lib().block_select_ex(B, H, kq, kk, d, _ptr(cq.contiguous()), _ptr(ck.contiguous()),
+                                     _ptr(offs_q), _ptr(offs_k), _ptr(budget), float(tau), float(theta),
+                                     int(rule), int(flags), _ptr(n_keep), _ptr(n_rows), _ptr(kept), w, wn,
+                                     _stream(cq)))
+        return n_keep, kept, n_rows
     _check(lib().block_select(B, H, kq, kk, d, _ptr(cq.contiguous()), _ptr(ck.contiguous()),
                               _ptr(offs_q), _ptr(offs_k), _ptr(budget), float(tau), float(theta),
                               int(rule), _ptr(n_keep), _ptr(kept), w, wn, _stream(cq)))
@@ -211,13 +229,20 @@ def block_select(cq, ck, offs_q, offs_k, budget, tau=0.95, theta=0.1, rule=RULE_
 
 
 def block_sparse_attn(q, k, v, perm_q, offs_q, perm_k, offs_k, n_keep, kept, scale=None,
-                      out=None, ws=None):
+                      out=None, ws=None, n_keep_rows=None):
+    """n_keep_rows [B,H,kq] (per-row counts from block_select(flags=SEL_PER_ROW)) -> the _ex entry."""
     _cuda(q, "q")
     B, H, N, d = q.shape
     kq, kk = offs_q.shape[-1] - 1, offs_k.shape[-1] - 1
     scale = d ** -0.5 if scale is None else scale
     out = torch.empty(B, H, N, d, dtype=torch.bfloat16, device=q.device) if out is None else out
     w, wn = _ws(ws, workspace_bytes(B, H, N, d, kq, kk), q.device)
+    if n_keep_rows is not None:
+        _check(lib().block_sparse_attn_ex(B, H, N, d, _bf16(q), _bf16(k), _bf16(v), kq, kk, _ptr(perm_q),
+                                          _ptr(offs_q), _ptr(perm_k), _ptr(offs_k), _ptr(n_keep),
+                                          _ptr(n_keep_rows), _ptr(kept), float(scale), _bf16(out, True), w, wn,
+                                          _stream(q)))
+        return out
     _check(lib().block_sparse_attn(B, H, N, d, _bf16(q), _bf16(k), _bf16(v), kq, kk, _ptr(perm_q),
                                    _ptr(offs_q), _ptr(perm_k), _ptr(offs_k), _ptr(n_keep),
                                    _ptr(kept), float(scale), _bf16(out, True), w, wn, _stream(q)))
@@ -226,11 +251,12 @@ def block_sparse_attn(q, k, v, perm_q, offs_q, perm_k, offs_k, n_keep, kept, sca
 
 def coclust_sparse_attention(q, k, v, kq, kk, iters, budget, *, seed=0, tau=0.95, theta=0.1,
                              rule=RULE_DENSITY, scale=None, out=None, ws=None, head_offset=0,
-                             heads_total=0, stage_events=None):
+                             heads_total=0, stage_events=None, sel_flags=0):
     """The whole SVOO attention layer (north_star stages 1-5) on device.
 
     stage_events: optional 4 torch.cuda.Event (enable_timing) recorded after co-clustering,
-    after selection, and around the attention kernel."""
+    after selection, and around the attention kernel.  sel_flags: SEL_* selection variants
+    (NEXT-4) -> coclust_sparse_attention_ex."""
     _cuda(q, "q")
     B, H, N, d = q.shape
     scale = d ** -0.5 if scale is None else scale
@@ -239,6 +265,12 @@ def coclust_sparse_attention(q, k, v, kq, kk, iters, budget, *, seed=0, tau=0.95
     evs = None
     if stage_events is not None:
         evs = (ctypes.c_void_p * 4)(*[ctypes.c_void_p(e.cuda_event) for e in stage_events])
+    if sel_flags:
+        _check(lib().coclust_sparse_attention_ex(B, H, N, d, _bf16(q), _bf16(k), _bf16(v), kq, kk, iters,
+                                                 seed, head_offset, heads_total, _ptr(budget), float(tau),
+                                                 float(theta), int(rule), int(sel_flags), float(scale),
+                                                 _bf16(out, True), w, wn, _stream(q), evs))
+        return out
     _check(lib().coclust_sparse_attention(B, H, N, d, _bf16(q), _bf16(k), _bf16(v), kq, kk, iters,
                                           seed, head_offset, heads_total, _ptr(budget), float(tau), float(theta), int(rule),
                                           float(scale), _bf16(out, True), w, wn, _stream(q), evs))
@@ -256,7 +288,7 @@ def block_transpose(src, A, B, out=None):
 
 class _LayerState(ctypes.Structure):
     _fields_ = [(n, ctypes.c_void_p) for n in ("cq", "ck", "lq", "lk", "perm_q", "perm_k", "offs_q",
-                                               "offs_k", "n_keep", "kept")]
+                                               "offs_k", "n_keep", "kept", "n_keep_rows")]
 
 
 class LayerState:
@@ -272,14 +304,15 @@ class LayerState:
         self.offs_k = torch.empty(B, H, kk + 1, **i32)
         self.n_keep = torch.empty(B, H, **i32)
         self.kept = torch.empty(B, H, kq, kk, **i32)
+        self.n_keep_rows = torch.empty(B, H, kq, **i32)
         self._c = _LayerState(*[t.data_ptr() for t in (self.cq, self.ck, self.lq, self.lk, self.perm_q,
                                                         self.perm_k, self.offs_q, self.offs_k, self.n_keep,
-                                                        self.kept)])
+                                                        self.kept, self.n_keep_rows)])
 
 
 def coclust_sparse_attention_cached(q, k, v, kq, kk, iters, budget, state, recompute, *, seed=0, tau=0.95,
                                     theta=0.1, rule=RULE_DENSITY, scale=None, out=None, ws=None,
-                                    head_offset=0, heads_total=0, stage_events=None):
+                                    head_offset=0, heads_total=0, stage_events=None, sel_flags=0):
     """The layer with clustering reuse: recompute=True refreshes `state`."""
     _cuda(q, "q")
     B, H, N, d = q.shape
@@ -291,7 +324,7 @@ def coclust_sparse_attention_cached(q, k, v, kq, kk, iters, budget, state, recom
         evs = (ctypes.c_void_p * 4)(*[ctypes.c_void_p(e.cuda_event) for e in stage_events])
     _check(lib().coclust_sparse_attention_cached(B, H, N, d, _bf16(q), _bf16(k), _bf16(v), kq, kk, iters,
                                                  seed, head_offset, heads_total, _ptr(budget), float(tau),
-                                                 float(theta), int(rule), float(scale), _bf16(out, True),
-                                                 ctypes.byref(state._c), int(bool(recompute)), w, wn,
+                                                 float(theta), int(rule), int(sel_flags), float(scale),
+                                                 _bf16(out, True), ctypes.byref(state._c), int(bool(recompute)), w, wn,
                                                  _stream(q), evs))
     return out

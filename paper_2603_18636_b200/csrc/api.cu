@@ -99,6 +99,7 @@ AttnScratch carve_attn(Carve& c, int BH, int N, int d, int kq) {
 struct LayerState {
   float *cq, *ck;
   int32_t *lq, *lk, *perm_q, *perm_k, *offs_q, *offs_k, *n_keep, *kept;
+  int32_t* n_rows;  // per-row kept counts [BH, kq] (nullable in the cached entry: shared n only)
 };
 LayerState carve_state(Carve& c, int BH, int N, int d, int kq, int kk) {
   LayerState s;
@@ -112,6 +113,7 @@ LayerState carve_state(Carve& c, int BH, int N, int d, int kq, int kk) {
   s.offs_k = c.take<int32_t>((size_t)BH * (kk + 1));
   s.n_keep = c.take<int32_t>((size_t)BH);
   s.kept = c.take<int32_t>((size_t)BH * kq * kk);
+  s.n_rows = c.take<int32_t>((size_t)BH * kq);
   return s;
 }
 
@@ -253,7 +255,7 @@ cs_status run_assign(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in k, int
 }
 
 cs_status run_attn(int B, int H, int N, int d, int kq, int kk, const int32_t* perm_q, const int32_t* offs_q,
-                   const int32_t* offs_k, const int32_t* n_keep, const int32_t* kept, float scale,
+                   const int32_t* offs_k, const int32_t* n_keep, const int32_t* n_rows, const int32_t* kept, float scale,
                    cs_bf16_out o, const AttnScratch& sc, cudaStream_t st, void* const* ev = nullptr) {
   const int BH = B * H;
   CS_CUDA(launch_worklist(BH, kq, offs_q, sc.item_start, st), "worklist");
@@ -265,7 +267,7 @@ cs_status run_attn(int B, int H, int N, int d, int kq, int kk, const int32_t* pe
     CS_CHECK(make_map_2d(&kv.v[i], sc.vp, (uint64_t)BH * N, d, 8u << i));
   }
   if (ev) CS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(ev[2]), st), "event");
-  CS_CUDA(launch_bsa_fwd(&tq, &kv, BH, H, N, d, kq, kk, perm_q, offs_q, offs_k, n_keep, kept,
+  CS_CUDA(launch_bsa_fwd(&tq, &kv, BH, H, N, d, kq, kk, perm_q, offs_q, offs_k, n_keep, n_rows, kept,
                          sc.item_start, worklist_upper_bound(N, kq), scale,
                          static_cast<__nv_bfloat16*>(o.ptr), o.sb, o.sh, o.sn, st),
           "bsa_fwd");
@@ -377,10 +379,10 @@ cs_status coclust_permute(int BH, int N, int k, const int32_t* labels, int32_t* 
   return CS_OK;
 }
 
-cs_status block_select(int B, int H, int kq, int kk, int d, const float* cq, const float* ck,
-                       const int32_t* offs_q, const int32_t* offs_k, const float* budget, double tau,
-                       double theta, int rule, int32_t* n_keep, int32_t* kept, void* ws, size_t ws_bytes,
-                       void* stream) {
+cs_status block_select_ex(int B, int H, int kq, int kk, int d, const float* cq, const float* ck,
+                          const int32_t* offs_q, const int32_t* offs_k, const float* budget, double tau,
+                          double theta, int rule, int flags, int32_t* n_keep, int32_t* n_keep_rows,
+                          int32_t* kept, void* ws, size_t ws_bytes, void* stream) {
   g_err[0] = 0;
   if (B <= 0 || H <= 0) return fail(CS_ERR_SHAPE, "B, H must be positive");
   if (d != 64 && d != 128) return fail(CS_ERR_SHAPE, "d must be 64 or 128 (got %d)", d);
@@ -389,22 +391,33 @@ cs_status block_select(int B, int H, int kq, int kk, int d, const float* cq, con
   if (!(tau > 0.0 && tau <= 1.0)) return fail(CS_ERR_ARG, "tau must be in (0, 1] (got %g)", tau);
   if (!(theta > 0.0 && theta < 1.0)) return fail(CS_ERR_ARG, "theta must be in (0, 1) (got %g)", theta);
   if (rule < 0 || rule > 2) return fail(CS_ERR_ARG, "unknown rule %d", rule);
+  if (flags & ~(CS_SEL_PER_ROW | CS_SEL_SIZE_WEIGHTED)) return fail(CS_ERR_ARG, "unknown selection flags 0x%x", flags);
   NEED(cq, "cq"); NEED(ck, "ck"); NEED(offs_q, "offs_q"); NEED(offs_k, "offs_k"); NEED(budget, "budget");
   NEED(n_keep, "n_keep"); NEED(kept, "kept");
+  if ((flags & CS_SEL_PER_ROW) && !n_keep_rows) return fail(CS_ERR_NULL, "n_keep_rows is NULL (CS_SEL_PER_ROW)");
   const int BH = B * H;
   CS_CHECK(check_ws(ws, ws_bytes, need_select(BH, kq, kk)));
   Carve c(ws);
   SelectScratch sc = carve_select(c, BH, kq, kk);
-  CS_CUDA(launch_block_select(BH, H, kq, kk, d, cq, ck, offs_q, offs_k, budget, tau, theta, rule, n_keep, kept,
-                              sc.order, sc.cnt, sc.abar, static_cast<cudaStream_t>(stream)),
+  CS_CUDA(launch_block_select(BH, H, kq, kk, d, cq, ck, offs_q, offs_k, budget, tau, theta, rule, flags, n_keep,
+                              n_keep_rows, kept, sc.order, sc.cnt, sc.abar, static_cast<cudaStream_t>(stream)),
           "block_select");
   return CS_OK;
 }
 
-cs_status block_sparse_attn(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in k, cs_bf16_in v, int kq, int kk,
-                            const int32_t* perm_q, const int32_t* offs_q, const int32_t* perm_k,
-                            const int32_t* offs_k, const int32_t* n_keep, const int32_t* kept, float scale,
-                            cs_bf16_out o, void* ws, size_t ws_bytes, void* stream) {
+cs_status block_select(int B, int H, int kq, int kk, int d, const float* cq, const float* ck,
+                       const int32_t* offs_q, const int32_t* offs_k, const float* budget, double tau,
+                       double theta, int rule, int32_t* n_keep, int32_t* kept, void* ws, size_t ws_bytes,
+                       void* stream) {
+  return block_select_ex(B, H, kq, kk, d, cq, ck, offs_q, offs_k, budget, tau, theta, rule, 0, n_keep, nullptr,
+                         kept, ws, ws_bytes, stream);
+}
+
+cs_status block_sparse_attn_ex(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in k, cs_bf16_in v, int kq,
+                               int kk, const int32_t* perm_q, const int32_t* offs_q, const int32_t* perm_k,
+                               const int32_t* offs_k, const int32_t* n_keep, const int32_t* n_keep_rows,
+                               const int32_t* kept, float scale, cs_bf16_out o, void* ws, size_t ws_bytes,
+                               void* stream) {
   g_err[0] = 0;
   CS_CHECK(check_dims(B, H, N, d));
   CS_CHECK(check_k(kq, N, "kq"));
@@ -424,7 +437,15 @@ cs_status block_sparse_attn(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in
   CS_CUDA(launch_permute_rows(view(q, H), BH, N, d, perm_q, sc.qp, st), "permute_q");
   CS_CUDA(launch_permute_rows(view(k, H), BH, N, d, perm_k, sc.kp, st), "permute_k");
   CS_CUDA(launch_permute_rows(view(v, H), BH, N, d, perm_k, sc.vp, st), "permute_v");
-  return run_attn(B, H, N, d, kq, kk, perm_q, offs_q, offs_k, n_keep, kept, scale, o, sc, st);
+  return run_attn(B, H, N, d, kq, kk, perm_q, offs_q, offs_k, n_keep, n_keep_rows, kept, scale, o, sc, st);
+}
+
+cs_status block_sparse_attn(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in k, cs_bf16_in v, int kq, int kk,
+                            const int32_t* perm_q, const int32_t* offs_q, const int32_t* perm_k,
+                            const int32_t* offs_k, const int32_t* n_keep, const int32_t* kept, float scale,
+                            cs_bf16_out o, void* ws, size_t ws_bytes, void* stream) {
+  return block_sparse_attn_ex(B, H, N, d, q, k, v, kq, kk, perm_q, offs_q, perm_k, offs_k, n_keep, nullptr, kept,
+                              scale, o, ws, ws_bytes, stream);
 }
 
 }  // extern "C"
@@ -432,7 +453,7 @@ cs_status block_sparse_attn(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in
 namespace {
 cs_status check_layer_args(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in k, cs_bf16_in v, int kq, int kk,
                            int iters, int& head_offset, int& heads_total, const float* budget, double tau,
-                           double theta, int rule, float scale, cs_bf16_out o) {
+                           double theta, int rule, int sel_flags, float scale, cs_bf16_out o) {
   CS_CHECK(check_dims(B, H, N, d));
   CS_CHECK(check_k(kq, N, "kq"));
   CS_CHECK(check_k(kk, N, "kk"));
@@ -440,6 +461,8 @@ cs_status check_layer_args(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in 
   if (!(tau > 0.0 && tau <= 1.0)) return fail(CS_ERR_ARG, "tau must be in (0, 1] (got %g)", tau);
   if (!(theta > 0.0 && theta < 1.0)) return fail(CS_ERR_ARG, "theta must be in (0, 1) (got %g)", theta);
   if (rule < 0 || rule > 2) return fail(CS_ERR_ARG, "unknown rule %d", rule);
+  if (sel_flags & ~(CS_SEL_PER_ROW | CS_SEL_SIZE_WEIGHTED))
+    return fail(CS_ERR_ARG, "unknown selection flags 0x%x", sel_flags);
   if (!(scale > 0.f)) return fail(CS_ERR_ARG, "scale must be > 0 (got %g)", (double)scale);
   CS_CHECK(check_heads(H, head_offset, heads_total));
   CS_CHECK(check_bf16(q.ptr, q.sb, q.sh, q.sn, "q"));
@@ -453,7 +476,7 @@ cs_status check_layer_args(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in 
 // The whole layer on device.  recompute: co-cluster + select into `s`; otherwise reuse `s`.
 cs_status run_layer(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in k, cs_bf16_in v, int kq, int kk,
                     int iters, uint64_t seed, int head_offset, int heads_total, const float* budget, double tau,
-                    double theta, int rule, float scale, cs_bf16_out o, const LayerState& s, bool recompute,
+                    double theta, int rule, int sel_flags, float scale, cs_bf16_out o, const LayerState& s, bool recompute,
                     Carve& c, cudaStream_t st, void* const* ev) {
   const int BH = B * H;
   AttnScratch at = carve_attn(c, BH, N, d, kq);
@@ -464,7 +487,7 @@ cs_status run_layer(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in k, cs_b
                         s.ck, s.lq, s.lk, s.perm_q, s.offs_q, s.perm_k, s.offs_k, as, at.qp, at.kp, st));
     if (ev) CS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(ev[0]), st), "event");
     CS_CUDA(launch_block_select(BH, H, kq, kk, d, s.cq, s.ck, s.offs_q, s.offs_k, budget, tau, theta, rule,
-                                s.n_keep, s.kept, se.order, se.cnt, se.abar, st),
+                                sel_flags, s.n_keep, s.n_rows, s.kept, se.order, se.cnt, se.abar, st),
             "block_select");
     if (ev) CS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(ev[1]), st), "event");
   } else {
@@ -475,37 +498,50 @@ cs_status run_layer(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in k, cs_b
     if (ev) CS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(ev[1]), st), "event");
   }
   CS_CUDA(launch_permute_rows(view(v, H), BH, N, d, s.perm_k, at.vp, st), "permute_v");
-  return run_attn(B, H, N, d, kq, kk, s.perm_q, s.offs_q, s.offs_k, s.n_keep, s.kept, scale, o, at, st, ev);
+  return run_attn(B, H, N, d, kq, kk, s.perm_q, s.offs_q, s.offs_k, s.n_keep, s.n_rows, s.kept, scale, o, at, st,
+                  ev);
 }
 }  // namespace
 
 extern "C" {
+
+cs_status coclust_sparse_attention_ex(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in k, cs_bf16_in v,
+                                      int kq, int kk, int iters, uint64_t seed, int head_offset, int heads_total,
+                                      const float* budget, double tau, double theta, int rule, int sel_flags,
+                                      float scale, cs_bf16_out o, void* ws, size_t ws_bytes, void* stream,
+                                      void* const* stage_events) {
+  g_err[0] = 0;
+  CS_CHECK(check_layer_args(B, H, N, d, q, k, v, kq, kk, iters, head_offset, heads_total, budget, tau, theta,
+                            rule, sel_flags, scale, o));
+  const int BH = B * H;
+  CS_CHECK(check_ws(ws, ws_bytes, need_layer(BH, N, d, kq, kk)));
+  Carve c(ws);
+  LayerState s = carve_state(c, BH, N, d, kq, kk);
+  return run_layer(B, H, N, d, q, k, v, kq, kk, iters, seed, head_offset, heads_total, budget, tau, theta, rule,
+                   sel_flags, scale, o, s, true, c, static_cast<cudaStream_t>(stream), stage_events);
+}
 
 cs_status coclust_sparse_attention(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in k, cs_bf16_in v, int kq,
                                    int kk, int iters, uint64_t seed, int head_offset, int heads_total,
                                    const float* budget, double tau, double theta,
                                    int rule, float scale, cs_bf16_out o, void* ws, size_t ws_bytes, void* stream,
                                    void* const* stage_events) {
-  g_err[0] = 0;
-  CS_CHECK(check_layer_args(B, H, N, d, q, k, v, kq, kk, iters, head_offset, heads_total, budget, tau, theta,
-                            rule, scale, o));
-  const int BH = B * H;
-  CS_CHECK(check_ws(ws, ws_bytes, need_layer(BH, N, d, kq, kk)));
-  Carve c(ws);
-  LayerState s = carve_state(c, BH, N, d, kq, kk);
-  return run_layer(B, H, N, d, q, k, v, kq, kk, iters, seed, head_offset, heads_total, budget, tau, theta, rule,
-                   scale, o, s, true, c, static_cast<cudaStream_t>(stream), stage_events);
+  return coclust_sparse_attention_ex(B, H, N, d, q, k, v, kq, kk, iters, seed, head_offset, heads_total, budget,
+                                     tau, theta, rule, 0, scale, o, ws, ws_bytes, stream, stage_events);
 }
 
 cs_status coclust_sparse_attention_cached(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in k, cs_bf16_in v,
                                           int kq, int kk, int iters, uint64_t seed, int head_offset,
                                           int heads_total, const float* budget, double tau, double theta, int rule,
-                                          float scale, cs_bf16_out o, const cs_layer_state* state, int recompute,
+                                          int sel_flags, float scale, cs_bf16_out o, const cs_layer_state* state,
+                                          int recompute,
                                           void* ws, size_t ws_bytes, void* stream, void* const* stage_events) {
   g_err[0] = 0;
   CS_CHECK(check_layer_args(B, H, N, d, q, k, v, kq, kk, iters, head_offset, heads_total, budget, tau, theta,
-                            rule, scale, o));
+                            rule, sel_flags, scale, o));
   NEED(state, "state");
+  if ((sel_flags & CS_SEL_PER_ROW) && !state->n_keep_rows)
+    return fail(CS_ERR_NULL, "state->n_keep_rows is NULL (CS_SEL_PER_ROW)");
   NEED(state->cq, "state->cq"); NEED(state->ck, "state->ck"); NEED(state->lq, "state->lq");
   NEED(state->lk, "state->lk"); NEED(state->perm_q, "state->perm_q"); NEED(state->offs_q, "state->offs_q");
   NEED(state->perm_k, "state->perm_k"); NEED(state->offs_k, "state->offs_k");
@@ -517,10 +553,10 @@ cs_status coclust_sparse_attention_cached(int B, int H, int N, int d, cs_bf16_in
   carve_select(dry, BH, kq, kk);
   CS_CHECK(check_ws(ws, ws_bytes, dry.off + 256));
   LayerState s{state->cq, state->ck, state->lq, state->lk, state->perm_q, state->perm_k, state->offs_q,
-               state->offs_k, state->n_keep, state->kept};
+               state->offs_k, state->n_keep, state->kept, state->n_keep_rows};
   Carve c(ws);
   return run_layer(B, H, N, d, q, k, v, kq, kk, iters, seed, head_offset, heads_total, budget, tau, theta, rule,
-                   scale, o, s, recompute != 0, c, static_cast<cudaStream_t>(stream), stage_events);
+                   sel_flags, scale, o, s, recompute != 0, c, static_cast<cudaStream_t>(stream), stage_events);
 }
 
 cs_status cs_block_transpose(int A, int B, size_t row_bytes, const void* src, void* dst, void* stream) {

@@ -70,7 +70,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     k_bsa_fwd(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ KVMaps kv, int H, int N,
               int kq, int kk, const int32_t* __restrict__ perm_q, const int32_t* __restrict__ offs_q,
               const int32_t* __restrict__ offs_k, const int32_t* __restrict__ n_keep,
-              const int32_t* __restrict__ kept, const int32_t* __restrict__ item_start,
+              const int32_t* __restrict__ n_rows, const int32_t* __restrict__ kept,
+              const int32_t* __restrict__ item_start,
               float scale_log2, __nv_bfloat16* __restrict__ out, long long osb, long long osh,
               long long osn) {
   using L = Smem<D>;
@@ -129,7 +130,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   if (warp == WARP_PRODUCER) {
     tma_prefetch_desc(&tm_q);
     if (lane < 5) { tma_prefetch_desc(&kv.k[lane]); tma_prefetch_desc(&kv.v[lane]); }
-    const int n = n_keep[bh];
+    const int n = n_rows ? n_rows[(size_t)bh * kq + a] : n_keep[bh];  // per-row counts (R11b)
     const int32_t* kl = kept + ((size_t)bh * kq + a) * kk;
     const int32_t* ok = offs_k + (size_t)bh * (kk + 1);
     int carry = 0;
@@ -553,7 +554,7 @@ extern "C" int cs_debug_attn_trace(void* host, size_t bytes) {
 cudaError_t launch_bsa_fwd(const CUtensorMap* tm_q, const KVMaps* kv,
                            int BH, int H, int N, int d, int kq, int kk, const int32_t* perm_q,
                            const int32_t* offs_q, const int32_t* offs_k, const int32_t* n_keep,
-                           const int32_t* kept, const int32_t* item_start, int items_ub,
+                           const int32_t* n_rows, const int32_t* kept, const int32_t* item_start, int items_ub,
                            float scale, __nv_bfloat16* o, long long osb, long long osh,
                            long long osn, cudaStream_t st) {
   const float scale_log2 = scale * 1.4426950408889634f;
@@ -564,14 +565,14 @@ cudaError_t launch_bsa_fwd(const CUtensorMap* tm_q, const KVMaps* kv,
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     kfn<<<grid, attn::NTHREADS, smem, st>>>(*tm_q, *kv, H, N, kq, kk, perm_q, offs_q, offs_k,
-                                           n_keep, kept, item_start, scale_log2, o, osb, osh, osn);
+                                           n_keep, n_rows, kept, item_start, scale_log2, o, osb, osh, osn);
   } else {
     auto kfn = attn::k_bsa_fwd<64>;
     const int smem = attn::Smem<64>::ALLOC;
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     kfn<<<grid, attn::NTHREADS, smem, st>>>(*tm_q, *kv, H, N, kq, kk, perm_q, offs_q, offs_k,
-                                           n_keep, kept, item_start, scale_log2, o, osb, osh, osn);
+                                           n_keep, n_rows, kept, item_start, scale_log2, o, osb, osh, osn);
   }
   return cudaGetLastError();
 }

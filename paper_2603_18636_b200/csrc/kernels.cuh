@@ -48,9 +48,9 @@ cudaError_t launch_assign_gemm(const CUtensorMap* tm_x, const CUtensorMap* tm_w,
 // ---- select.cu
 cudaError_t launch_block_select(int BH, int H, int kq, int kk, int d, const float* cq,
                                 const float* ck, const int32_t* offs_q, const int32_t* offs_k,
-                                const float* budget, double tau, double theta, int rule,
-                                int32_t* n_keep, int32_t* kept, int32_t* order, int32_t* cnt,
-                                double* abar, cudaStream_t st);
+                                const float* budget, double tau, double theta, int rule, int flags,
+                                int32_t* n_keep, int32_t* n_rows, int32_t* kept, int32_t* order,
+                                int32_t* cnt, double* abar, cudaStream_t st);
 cudaError_t launch_worklist(int BH, int kq, const int32_t* offs_q, int32_t* item_start,
                             cudaStream_t st);
 int worklist_upper_bound(int N, int kq);
@@ -64,7 +64,7 @@ struct KVMaps {
 cudaError_t launch_bsa_fwd(const CUtensorMap* tm_q, const KVMaps* kv,
                            int BH, int H, int N, int d, int kq, int kk, const int32_t* perm_q,
                            const int32_t* offs_q, const int32_t* offs_k, const int32_t* n_keep,
-                           const int32_t* kept, const int32_t* item_start, int items_ub,
+                           const int32_t* n_rows, const int32_t* kept, const int32_t* item_start, int items_ub,
                            float scale, __nv_bfloat16* o, long long osb, long long osh,
                            long long osn, cudaStream_t st);
 

@@ -130,7 +130,8 @@ template <int E>
 __global__ void __launch_bounds__(256) k_select_rows(int kq, int kk, int d, const double* __restrict__ abar,
                                                      const int32_t* __restrict__ offs_q,
                                                      const int32_t* __restrict__ offs_k, double tau,
-                                                     int32_t* __restrict__ order, int32_t* __restrict__ cnt) {
+                                                     int weighted, int32_t* __restrict__ order,
+                                                     int32_t* __restrict__ cnt) {
   extern __shared__ double sh_d[];
   __shared__ double wred[8];
   __shared__ int first_hit;
@@ -143,14 +144,17 @@ __global__ void __launch_bounds__(256) k_select_rows(int kq, int kk, int d, cons
   const int32_t* oq = offs_q + (size_t)bh * (kq + 1);
   (void)scq;
   const double* arow = abar + ((size_t)bh * kq + a) * kk;
-  // sort: (value desc, index asc); empty key blocks and padding are -inf
+  // sort: (value desc, index asc); empty key blocks and padding are -inf.  The value is the raw
+  // Abar (R7), or with CS_SEL_SIZE_WEIGHTED the importance Abar / sqrt(d) + log|K_c| (R9c).
+  const double sdiv = weighted ? 1.0 : sqrt((double)d);  // softmax argument = value / sdiv
   {
     double v[E];
     int ix[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       const int j = t * E + e;
-      v[e] = (j < kk && ok[j + 1] - ok[j] > 0) ? arow[j] : -INFINITY;
+      const int sz = j < kk ? ok[j + 1] - ok[j] : 0;
+      v[e] = sz > 0 ? (weighted ? arow[j] / sqrt((double)d) + log((double)sz) : arow[j]) : -INFINITY;
       ix[e] = j;
     }
     bitonic_sort_rows<E>(v, ix, P2, sval, sidx);
@@ -172,7 +176,7 @@ __global__ void __launch_bounds__(256) k_select_rows(int kq, int kk, int d, cons
     return;
   }
   // softmax over the kne nonempty entries (sorted prefix), then the cumulative mass
-  const double sd = sqrt((double)d);
+  const double sd = sdiv;
   const double mz = sval[0] / sd;
   // each thread owns 4 consecutive sorted entries (P2 <= 1024)
   constexpr int per = E;
@@ -220,14 +224,27 @@ __device__ __forceinline__ int n_from_ratio(double r, int kk) {
   return min(max(n, 1), kk);
 }
 
-// grid BH, block 1024
+// the rho rule (R8, R10) for a recall count n_rec, clamped to [1, K_k']
+__device__ __forceinline__ int rule_n(int n_rec, double b, double theta, int rule, int kk, int nk) {
+  const int n_b = n_from_ratio(b, kk);
+  int n;
+  if (rule == 0) n = (1.0 - b) > theta ? min(n_rec, n_b) : max(n_rec, n_b);
+  else if (rule == 1) n = b > theta ? min(n_rec, n_b) : max(n_rec, n_b);
+  else n = n_b;
+  return min(max(n, 1), max(nk, 1));
+}
+
+// grid BH, block 1024.  n_keep[bh] = rule(n_rec) (R11).  n_rows (optional) gets the per-row
+// counts: with per_row (CS_SEL_PER_ROW, R11b) rule(c_a) for nonempty query blocks and the shared
+// n for empty ones; without it the shared n everywhere.
 __global__ void __launch_bounds__(1024) k_select_count(int H, int kq, int kk,
                                                        const int32_t* __restrict__ offs_q,
                                                        const int32_t* __restrict__ offs_k,
                                                        const int32_t* __restrict__ cnt,
                                                        const float* __restrict__ budget, double theta,
-                                                       int rule, int32_t* __restrict__ n_keep) {
-  __shared__ int s_sum[32], s_nq[32], s_nk[32];
+                                                       int rule, int per_row, int32_t* __restrict__ n_keep,
+                                                       int32_t* __restrict__ n_rows) {
+  __shared__ int s_sum[32], s_nq[32], s_nk[32], s_n, s_NK;
   const int bh = blockIdx.x, t = threadIdx.x;
   const int32_t* oq = offs_q + (size_t)bh * (kq + 1);
   const int32_t* ok = offs_k + (size_t)bh * (kk + 1);
@@ -239,29 +256,32 @@ __global__ void __launch_bounds__(1024) k_select_count(int H, int kq, int kk,
   sum = warp_sum(sum); nq = warp_sum(nq); nk = warp_sum(nk);
   if ((t & 31) == 0) { s_sum[t >> 5] = sum; s_nq[t >> 5] = nq; s_nk[t >> 5] = nk; }
   __syncthreads();
+  const double b = (double)budget[bh % H];
   if (t == 0) {
     int S = 0, NQ = 0, NK = 0;
     for (int w = 0; w < 32; ++w) { S += s_sum[w]; NQ += s_nq[w]; NK += s_nk[w]; }
     const int n_rec = NQ > 0 ? (S + NQ - 1) / NQ : 1;
-    const double b = (double)budget[bh % H];
-    const int n_b = n_from_ratio(b, kk);
-    int n;
-    if (rule == 0) n = (1.0 - b) > theta ? min(n_rec, n_b) : max(n_rec, n_b);
-    else if (rule == 1) n = b > theta ? min(n_rec, n_b) : max(n_rec, n_b);
-    else n = n_b;
-    n = min(max(n, 1), max(NK, 1));
+    const int n = rule_n(n_rec, b, theta, rule, kk, NK);
     n_keep[bh] = n;
+    s_n = n;
+    s_NK = NK;
   }
+  if (!n_rows) return;
+  __syncthreads();
+  for (int a = t; a < kq; a += 1024)
+    n_rows[(size_t)bh * kq + a] = (per_row && oq[a + 1] - oq[a] > 0)
+                                      ? rule_n(cnt[(size_t)bh * kq + a], b, theta, rule, kk, s_NK) : s_n;
 }
 
 // grid (kq, BH), block 256: kept row = first n of order, ascending
 __global__ void __launch_bounds__(256) k_select_emit(int kq, int kk, const int32_t* __restrict__ order,
                                                      const int32_t* __restrict__ n_keep,
+                                                     const int32_t* __restrict__ n_rows,
                                                      int32_t* __restrict__ kept) {
   __shared__ uint32_t flags[kMaxClusters / 32];
   __shared__ int sbuf[32];
   const int a = blockIdx.x, bh = blockIdx.y, t = threadIdx.x;
-  const int n = n_keep[bh];
+  const int n = n_rows ? n_rows[(size_t)bh * kq + a] : n_keep[bh];
   for (int w = t; w < kMaxClusters / 32; w += 256) flags[w] = 0u;
   __syncthreads();
   const int32_t* ord = order + ((size_t)bh * kq + a) * kk;
@@ -321,9 +341,10 @@ int worklist_upper_bound(int N, int kq) { return (N + 255) / 256 + kq; }
 
 cudaError_t launch_block_select(int BH, int H, int kq, int kk, int d, const float* cq,
                                 const float* ck, const int32_t* offs_q, const int32_t* offs_k,
-                                const float* budget, double tau, double theta, int rule,
-                                int32_t* n_keep, int32_t* kept, int32_t* order, int32_t* cnt,
-                                double* abar, cudaStream_t st) {
+                                const float* budget, double tau, double theta, int rule, int flags,
+                                int32_t* n_keep, int32_t* n_rows, int32_t* kept, int32_t* order,
+                                int32_t* cnt, double* abar, cudaStream_t st) {
+  const int weighted = (flags & 2) ? 1 : 0;
   int P2 = 256;
   while (P2 < kk) P2 <<= 1;
   const size_t smem = (size_t)P2 * 8 + (size_t)d * 8 + (size_t)P2 * 4;
@@ -340,13 +361,14 @@ cudaError_t launch_block_select(int BH, int H, int kq, int kk, int d, const floa
     k_abar<64><<<gab, 256, sab, st>>>(kq, kk, cq, ck, abar);
   }
   if (P2 == 256)
-    k_select_rows<1><<<dim3(kq, BH), 256, smem, st>>>(kq, kk, d, abar, offs_q, offs_k, tau, order, cnt);
+    k_select_rows<1><<<dim3(kq, BH), 256, smem, st>>>(kq, kk, d, abar, offs_q, offs_k, tau, weighted, order, cnt);
   else if (P2 == 512)
-    k_select_rows<2><<<dim3(kq, BH), 256, smem, st>>>(kq, kk, d, abar, offs_q, offs_k, tau, order, cnt);
+    k_select_rows<2><<<dim3(kq, BH), 256, smem, st>>>(kq, kk, d, abar, offs_q, offs_k, tau, weighted, order, cnt);
   else
-    k_select_rows<4><<<dim3(kq, BH), 256, smem, st>>>(kq, kk, d, abar, offs_q, offs_k, tau, order, cnt);
-  k_select_count<<<BH, 1024, 0, st>>>(H, kq, kk, offs_q, offs_k, cnt, budget, theta, rule, n_keep);
-  k_select_emit<<<dim3(kq, BH), 256, 0, st>>>(kq, kk, order, n_keep, kept);
+    k_select_rows<4><<<dim3(kq, BH), 256, smem, st>>>(kq, kk, d, abar, offs_q, offs_k, tau, weighted, order, cnt);
+  k_select_count<<<BH, 1024, 0, st>>>(H, kq, kk, offs_q, offs_k, cnt, budget, theta, rule, flags & 1, n_keep,
+                                      n_rows);
+  k_select_emit<<<dim3(kq, BH), 256, 0, st>>>(kq, kk, order, n_keep, n_rows, kept);
   return cudaGetLastError();
 }
 

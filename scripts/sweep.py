@@ -40,27 +40,29 @@ def peaks():
     return d.get("bf16_tflops_sustained", 1400.0), d.get("bf16_tflops", 1590.0)
 
 
-def kept_flops(q, k, kq, kk, iters, budget, tau, theta, rule, seed, ws):
+def kept_flops(q, k, kq, kk, iters, budget, tau, theta, rule, seed, ws, flags=0):
     """F_kept of one layer, from the staged entries (same kernels and bits as the fused call)."""
     st = pb.coclust_assign(q, k, kq, kk, iters, seed=seed, ws=ws)
-    n_keep, kept = pb.block_select(st["cq"], st["ck"], st["offs_q"], st["offs_k"], budget, tau, theta, rule,
-                                   ws=ws)
+    sel = pb.block_select(st["cq"], st["ck"], st["offs_q"], st["offs_k"], budget, tau, theta, rule, ws=ws,
+                          flags=flags)
+    n_keep, kept = sel[0], sel[1]
     B, H, N, d = q.shape
     oq = st["offs_q"].cpu().numpy().reshape(B * H, -1)
     ok = st["offs_k"].cpu().numpy().reshape(B * H, -1)
     kp = kept.cpu().numpy().reshape(B * H, kq, kk)
     nk = n_keep.cpu().numpy().reshape(-1)
+    nrows = sel[2].cpu().numpy().reshape(B * H, kq) if flags else np.repeat(nk[:, None], kq, 1)
     f = 0
     for bh in range(B * H):
         sq, sk = np.diff(oq[bh]), np.diff(ok[bh])
-        f += int((sq * sk[kp[bh, :, :nk[bh]]].sum(1)).sum())
+        f += sum(int(sq[a]) * int(sk[kp[bh, a, :nrows[bh, a]]].sum()) for a in range(kq))
     return 4 * d * f, nk
 
 
-def time_layer(q, k, v, kq, kk, iters, budget, tau, theta, rule, seed, ws, out, warmup, steps):
+def time_layer(q, k, v, kq, kk, iters, budget, tau, theta, rule, seed, ws, out, warmup, steps, flags=0):
     for _ in range(warmup):
         pb.coclust_sparse_attention(q, k, v, kq, kk, iters, budget, seed=seed, tau=tau, theta=theta, rule=rule,
-                                    out=out, ws=ws)
+                                    out=out, ws=ws, sel_flags=flags)
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(steps)]
     for e in (x for row in evs for x in row):
         e.record()
@@ -69,7 +71,7 @@ def time_layer(q, k, v, kq, kk, iters, budget, tau, theta, rule, seed, ws, out, 
     for i in range(steps):
         starts[i].record()
         pb.coclust_sparse_attention(q, k, v, kq, kk, iters, budget, seed=seed, tau=tau, theta=theta, rule=rule,
-                                    out=out, ws=ws, stage_events=evs[i])
+                                    out=out, ws=ws, stage_events=evs[i], sel_flags=flags)
     starts[steps].record()
     torch.cuda.synchronize()
     ms = starts[0].elapsed_time(starts[steps]) / steps
@@ -139,9 +141,10 @@ def run_layers(a):
         B, H, N, d = q.shape
         out = torch.empty_like(q)
         budget = prof[layer].to(dev)
-        fk, nk = kept_flops(q, k, c["kq"], c["kk"], c["iters"], budget, a.tau, a.theta, RULES["density"], a.seed, ws)
+        fk, nk = kept_flops(q, k, c["kq"], c["kk"], c["iters"], budget, a.tau, a.theta, RULES["density"], a.seed, ws,
+                            a.sel_flags)
         ms, stg = time_layer(q, k, v, c["kq"], c["kk"], c["iters"], budget, a.tau, a.theta, RULES["density"], a.seed,
-                             ws, out, a.warmup, a.steps)
+                             ws, out, a.warmup, a.steps, a.sel_flags)
         dense = 4.0 * B * H * N * N * d
         ach = fk / (stg["attention"] * 1e-3) / 1e12
         row = {"layer": layer, "budget_mean": float(budget.mean()), "n_keep": [int(x) for x in nk],
@@ -156,7 +159,8 @@ def run_layers(a):
         del w, q, k, v, out
     ms = np.array([r["ms_layer"] for r in rows])
     fr = np.array([r["roofline_frac_sustained"] for r in rows])
-    summ = {"config": a.config, "rule": "density", "tau": a.tau, "theta": a.theta, "layers": nl,
+    summ = {"config": a.config, "rule": "density", "tau": a.tau, "theta": a.theta, "sel_flags": a.sel_flags,
+            "layers": nl,
             "ms_layer_mean": float(ms.mean()), "ms_layer_min": float(ms.min()), "ms_layer_max": float(ms.max()),
             "ms_layer_mean_excl_dense_layer0": float(ms[1:].mean()) if nl > 1 else None,
             "kept_frac_mean": float(np.mean([r["kept_frac"] for r in rows])),
@@ -178,6 +182,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--sel-flags", type=int, default=0, help="NEXT-4 selection variants (layers mode)")
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
     t0 = time.time()

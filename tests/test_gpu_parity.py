@@ -174,6 +174,85 @@ def test_block_select_bitexact(pb, rule, kq, kk, d, tau):
         assert np.array_equal(kept[0, h, :, :ref.n_keep].cpu().numpy(), ref.kept)
 
 
+def _margins_ok_z(Cq, Ck, sq, sk, tau, d, weighted):
+    """_margins_ok on the ranking values of the NEXT-4 variants (z = Abar/sqrt(d) + log|K_c|)."""
+    A = Cq @ Ck.T / math.sqrt(d) + (np.log(np.maximum(sk, 1)) if weighted else 0.0)
+    for a in range(A.shape[0]):
+        v = np.sort(A[a, sk > 0])[::-1]
+        if len(v) > 1 and np.min(np.abs(np.diff(v)) / np.maximum(np.abs(v[:-1]), 1e-300)) < 1e-9:
+            return False
+        if sq[a] > 0:
+            p = svoo.softmax_row(v)
+            if np.min(np.abs(np.cumsum(p) - (tau - 1e-12))) < 1e-12:
+                return False
+    return True
+
+
+@pytest.mark.parametrize("flags", [1, 2, 3])
+@pytest.mark.parametrize("rule", [svoo.RULE_DENSITY, svoo.RULE_FIXED])
+@pytest.mark.parametrize("kq,kk,d,tau", [(16, 16, 64, 0.95), (100, 500, 128, 0.95), (256, 1024, 128, 0.6)])
+def test_block_select_variants_bitexact(pb, flags, rule, kq, kk, d, tau):
+    """NEXT-4: per-row counts (R11b) and size-weighted importance (R9c): n_keep, the per-row
+    counts and every kept row bit-exact against the oracle."""
+    H = 3
+    budget = torch.tensor([0.05, 0.3, 0.97], dtype=torch.float32)
+    theta = 0.1
+    seed = kq * 11 + kk + flags
+    while True:
+        g = torch.Generator().manual_seed(seed)
+        Cq = torch.randn(1, H, kq, d, generator=g) * 0.3
+        Ck = torch.randn(1, H, kk, d, generator=g) * 0.3
+        sq = torch.randint(0, 4, (H, kq), generator=g)
+        sk = torch.randint(0, 6, (H, kk), generator=g)
+        sq[:, 0] = 1
+        sk[:, 0] = 1
+        if all(_margins_ok_z(Cq[0, h].double().numpy(), Ck[0, h].double().numpy(), sq[h].numpy(),
+                             sk[h].numpy(), tau, d, flags & 2) for h in range(H)):
+            break
+        seed += 1000
+    offs_q = torch.cat([torch.zeros(H, 1, dtype=torch.long), sq.cumsum(1)], 1).int()[None]
+    offs_k = torch.cat([torch.zeros(H, 1, dtype=torch.long), sk.cumsum(1)], 1).int()[None]
+    n_keep, kept, n_rows = pb.block_select(Cq.cuda(), Ck.cuda(), offs_q.cuda(), offs_k.cuda(), budget.cuda(),
+                                           tau, theta, rule, flags=flags)
+    torch.cuda.synchronize()
+    for h in range(H):
+        ref = svoo.select_blocks(Cq[0, h].double().numpy(), Ck[0, h].double().numpy(), sq[h].numpy(),
+                                 sk[h].numpy(), float(budget[h]), tau, theta, rule, d_head=d,
+                                 per_row=bool(flags & 1), size_weighted=bool(flags & 2))
+        assert n_keep[0, h].item() == ref.n_keep
+        rows = ref.n_rows if flags & 1 else np.full(kq, ref.n_keep)
+        assert np.array_equal(n_rows[0, h].cpu().numpy(), rows)
+        for a in range(kq):
+            assert np.array_equal(kept[0, h, a, :rows[a]].cpu().numpy(), np.asarray(ref.kept[a]))
+
+
+def test_attn_per_row_counts_and_fused_variants(pb):
+    """Attention over per-row kept counts (R11b) against the oracle, and the fused entry with
+    selection flags bit-equal to the staged entries."""
+    w = video_qkv(6, 24, 40, 2, 128, seed=13)        # N = 5760
+    kq, kk, iters, tau, theta = 40, 120, 2, 0.9, 0.1
+    budget = torch.tensor([0.15, 0.35], dtype=torch.float32).cuda()
+    q, k, v = w.q.cuda(), w.k.cuda(), w.v.cuda()
+    for flags in (1, 3):
+        st = pb.coclust_assign(q, k, kq, kk, iters, seed=3)
+        n_keep, kept, n_rows = pb.block_select(st["cq"], st["ck"], st["offs_q"], st["offs_k"], budget, tau, theta,
+                                               pb.RULE_DENSITY, flags=flags)
+        o = pb.block_sparse_attn(q, k, v, st["perm_q"], st["offs_q"], st["perm_k"], st["offs_k"], n_keep, kept,
+                                 n_keep_rows=n_rows)
+        of = pb.coclust_sparse_attention(q, k, v, kq, kk, iters, budget, seed=3, tau=tau, theta=theta,
+                                         rule=pb.RULE_DENSITY, sel_flags=flags)
+        torch.cuda.synchronize()
+        assert torch.equal(o, of)
+        nr = n_rows.cpu().numpy()
+        assert len(np.unique(nr)) > 1        # the rows really differ
+        for h in range(2):
+            rows = [kept[0, h, a, :nr[0, h, a]].cpu().numpy() for a in range(kq)]
+            ref = svoo.sparse_attention(f64(w.q[0, h]), f64(w.k[0, h]), f64(w.v[0, h]),
+                                        st["lq"][0, h].cpu().numpy(), st["lk"][0, h].cpu().numpy(), rows)
+            err = np.abs(f64(o[0, h]) - ref)
+            assert err.max() <= ATOL_MAX and err.mean() <= ATOL_MEAN
+
+
 # ------------------------------------------------------------------------- P5 attention
 def _oracle_state(w, kq, kk, seed, budget, rule, tau=0.95, theta=0.1, heads=None):
     """Run the oracle's co-clustering + selection per head; returns GPU-ready int32 tensors."""
