@@ -28,6 +28,10 @@ Functions and their pins (tests/test_oracle_*.py):
                                                           size-weighted masses, hand example
   sparse_attention                          P:1257        pinned: ρ=1 == library SDPA, singleton
                                                           case, n=8 brute force, convexity
+  kmeans / cocluster_kmeans ("w/o On")      P:1058, P:1270 pinned: sklearn KMeans (lloyd, same init),
+                                                          Lloyd objective non-increasing
+  reference_pairs / block_pair_* (recall)   P:181-183     pinned: brute-force minimal prefix,
+                                                          identity / single-block partitions
 """
 from __future__ import annotations
 
@@ -200,6 +204,61 @@ def cocluster(Q: np.ndarray, K: np.ndarray, kq: int, kk: int, iters: int, *,
                           C_new=Cq_new, J=rb.objective))
         Ck, Cq = Ck_new, Cq_new
         Lk, Lq = ra.labels, rb.labels
+    return CoclusterResult(Lq, Cq, Lk, Ck, trace)
+
+
+# ----------------------------------------------------------------------------------------------
+# Independent k-means baseline ("w/o On" ablation; SVG2's partitioning, P:1270-1273;
+# SURVEY §8f NEXT-2).  Queries and keys are clustered separately by Lloyd's algorithm in raw
+# token space, initialised by the same sampler (R4).
+# ----------------------------------------------------------------------------------------------
+def kmeans_step(X: np.ndarray, C: np.ndarray) -> AssignResult:
+    """L(i) = argmin_j ||x_i - c_j||_2 (ties -> lowest j); gap / objective as in assign_step."""
+    X = np.asarray(X, np.float64)
+    C = np.asarray(C, np.float64)
+    sq = (X * X).sum(1)[:, None] + (C * C).sum(1)[None, :] - 2.0 * (X @ C.T)
+    D = np.sqrt(np.maximum(sq, 0.0))
+    labels = np.argmin(D, axis=1)
+    N, K = D.shape
+    d1 = D[np.arange(N), labels]
+    if K > 1:
+        D2 = D.copy()
+        D2[np.arange(N), labels] = np.inf
+        d2 = D2.min(axis=1)
+        gap = (d2 - d1) / np.maximum(d2, 1e-300)
+    else:
+        gap = np.full(N, np.inf)
+    return AssignResult(labels.astype(np.int64), gap, d1, float((d1 * d1).sum()))
+
+
+def kmeans(X: np.ndarray, K: int, iters: int, *, seed: int = 0, b: int = 0, h: int = 0, H: int = 1,
+           side: int = 0, init: np.ndarray | None = None):
+    """Lloyd: C^(0) = X[Sample(X, K)] (R4, stream `side`); repeat iters times: assign, then
+    C_j = mean of members (empty keeps its previous row, R5).  Returns (labels, C, trace) with the
+    Lloyd objective sum_i ||x_i - c_L(i)||^2 of every assignment in trace."""
+    X = np.asarray(X, np.float64)
+    idx = init if init is not None else sample_anchor_indices(X.shape[0], K, seed, b, h, H, side)
+    C = X[np.asarray(idx)].copy()
+    trace = []
+    labels = None
+    for it in range(iters):
+        r = kmeans_step(X, C)
+        C_new = update_centroids(X, r.labels, C)
+        trace.append(dict(it=it, labels=r.labels, gap=r.gap, C_self=C, C_new=C_new, J=r.objective))
+        C, labels = C_new, r.labels
+    return labels, C, trace
+
+
+def cocluster_kmeans(Q: np.ndarray, K: np.ndarray, kq: int, kk: int, iters: int, *, seed: int = 0,
+                     b: int = 0, h: int = 0, H: int = 1, init_q=None, init_k=None) -> CoclusterResult:
+    """The "w/o On" partitioning: independent k-means of K (K_k clusters) and Q (K_q clusters),
+    same sampler streams as Alg. 1 (keys side 1, queries side 0); same result type as cocluster."""
+    Lk, Ck, tk = kmeans(K, kk, iters, seed=seed, b=b, h=h, H=H, side=1, init=init_k)
+    Lq, Cq, tq = kmeans(Q, kq, iters, seed=seed, b=b, h=h, H=H, side=0, init=init_q)
+    trace = []
+    for a, c in zip(tk, tq):
+        trace.append(dict(side="k", **a))
+        trace.append(dict(side="q", **c))
     return CoclusterResult(Lq, Cq, Lk, Ck, trace)
 
 
@@ -410,3 +469,46 @@ def kept_flops(offs_q: np.ndarray, offs_k: np.ndarray, kept: np.ndarray, d: int)
     for a in range(len(sq)):
         tot += int(sq[a]) * int(sk[np.asarray(kept[a])].sum())
     return 4 * d * tot
+
+
+# ----------------------------------------------------------------------------------------------
+# Matched-budget attention recall (R19)
+# ----------------------------------------------------------------------------------------------
+def reference_pairs(A: np.ndarray, mass: float = 0.5) -> np.ndarray:
+    """The high-attention reference set: sort all token pairs by A_ij (desc) and take the
+    smallest prefix whose cumulative attention mass reaches `mass` of the total.  Returns a
+    boolean [N, N] mask.  A is the dense attention matrix (rows sum to 1)."""
+    A = np.asarray(A, np.float64)
+    flat = A.ravel()
+    order = np.argsort(-flat, kind="stable")
+    cs = np.cumsum(flat[order])
+    m = int(np.searchsorted(cs, mass * cs[-1], side="left")) + 1
+    mask = np.zeros(flat.shape, dtype=bool)
+    mask[order[:m]] = True
+    return mask.reshape(A.shape)
+
+
+def block_pair_counts(ref: np.ndarray, Lq: np.ndarray, Lk: np.ndarray, kq: int, kk: int) -> np.ndarray:
+    """cnt[a, c] = #{(i, j) in ref : L_q(i) = a, L_k(j) = c}: reference pairs covered by the block
+    pair (a, c) ("a token pair is covered if its query token and key token fall into the
+    selected Q-K block pair")."""
+    cnt = np.zeros((kq, kk), dtype=np.int64)
+    ii, jj = np.nonzero(ref)
+    np.add.at(cnt, (np.asarray(Lq)[ii], np.asarray(Lk)[jj]), 1)
+    return cnt
+
+
+def block_pair_recall(cnt: np.ndarray, budget_pairs: int) -> float:
+    """Recall of the reference set with `budget_pairs` block pairs, each method choosing its best
+    pairs (most covered reference pairs first, ties -> lowest flat index)."""
+    flat = cnt.ravel()
+    order = np.argsort(-flat, kind="stable")
+    tot = int(flat.sum())
+    return float(flat[order[:budget_pairs]].sum()) / tot if tot else 1.0
+
+
+def pairs_to_cover(cnt: np.ndarray, frac: float = 1.0) -> int:
+    """Fewest block pairs whose covered reference pairs reach `frac` of the reference set."""
+    flat = np.sort(cnt.ravel())[::-1]
+    cs = np.cumsum(flat)
+    return int(np.searchsorted(cs, frac * cs[-1] - 1e-9, side="left")) + 1

@@ -418,3 +418,67 @@ def test_per_row_empty_query_block_keeps_shared_n():
         if sq[a] > 0:
             assert pr.n_rows[a] == svoo.rule_count(int(pr.c[a]), 0.2, 0.1, svoo.RULE_DENSITY, len(sk),
                                                    int((sk > 0).sum()))
+
+
+# ------------------------------------------------------------------ NEXT-2 k-means baseline + recall
+def _blobs(n_per, centers, seed, sd=0.3):
+    rng = np.random.default_rng(seed)
+    X = np.concatenate([c + sd * rng.normal(size=(n_per, len(c))) for c in centers])
+    return X, np.repeat(np.arange(len(centers)), n_per)
+
+
+def test_kmeans_matches_sklearn_lloyd():
+    """Independent k-means (the "w/o On" partitioning) = textbook Lloyd: sklearn's KMeans
+    (algorithm="lloyd", the same initial centroids, n_init=1) reaches the same centroids."""
+    from sklearn.cluster import KMeans
+    rng = np.random.default_rng(3)
+    centers = rng.normal(size=(6, 8)) * 3
+    X, _ = _blobs(40, centers, 4, sd=1.0)
+    init = np.array([0, 45, 90, 130, 170, 230])     # one token per blob: no empty cluster
+    for iters in (1, 2, 5):
+        L, C, _ = svoo.kmeans(X, 6, iters, init=init)
+        km = KMeans(n_clusters=6, init=X[init], n_init=1, max_iter=iters, algorithm="lloyd", tol=0.0).fit(X)
+        assert np.allclose(C, km.cluster_centers_, atol=1e-10)
+        # our labels are those of the last assignment (R13); sklearn's of its final E-step
+        assert np.array_equal(svoo.kmeans_step(X, C).labels, km.labels_)
+
+
+def test_kmeans_objective_nonincreasing_and_recovers_blobs():
+    rng = np.random.default_rng(5)
+    centers = rng.normal(size=(5, 16)) * 4
+    X, truth = _blobs(50, centers, 6)
+    L, C, tr = svoo.kmeans(X, 5, 6, seed=1)
+    J = [t["J"] for t in tr]
+    assert all(J[i + 1] <= J[i] + 1e-9 for i in range(len(J) - 1))
+    # well-separated blobs seeded one token per blob: the partition is the truth up to relabelling
+    L2, _, _ = svoo.kmeans(X, 5, 3, init=np.arange(5) * 50 + 7)
+    assert len({(a, b) for a, b in zip(L2, truth)}) == 5 and len(np.unique(L2)) == 5
+
+
+def test_reference_pairs_minimal_prefix_bruteforce():
+    rng = np.random.default_rng(7)
+    S = rng.normal(size=(6, 6)) * 2
+    A = np.exp(S - S.max(1, keepdims=True))
+    A /= A.sum(1, keepdims=True)
+    ref = svoo.reference_pairs(A, 0.5)
+    assert A[ref].sum() >= 0.5 * A.sum() - 1e-12
+    # minimality: dropping the smallest selected pair goes below the target, and every unselected
+    # pair is no larger than every selected one
+    assert A[ref].sum() - A[ref].min() < 0.5 * A.sum()
+    assert A[~ref].max() <= A[ref].min()
+
+
+def test_block_pair_recall_special_partitions():
+    rng = np.random.default_rng(8)
+    S = rng.normal(size=(12, 12))
+    A = np.exp(S) / np.exp(S).sum(1, keepdims=True)
+    ref = svoo.reference_pairs(A, 0.5)
+    n = int(ref.sum())
+    ident = np.arange(12)
+    cnt = svoo.block_pair_counts(ref, ident, ident, 12, 12)
+    assert np.array_equal(cnt, ref.astype(np.int64))
+    assert svoo.pairs_to_cover(cnt) == n and svoo.block_pair_recall(cnt, n) == 1.0
+    assert svoo.block_pair_recall(cnt, n - 1) == (n - 1) / n
+    one = np.zeros(12, int)
+    cnt1 = svoo.block_pair_counts(ref, one, one, 1, 1)
+    assert cnt1[0, 0] == n and svoo.block_pair_recall(cnt1, 1) == 1.0 and svoo.pairs_to_cover(cnt1) == 1
