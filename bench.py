@@ -49,7 +49,8 @@ def parse():
     ap.add_argument("--reuse-steps", type=int, default=1,
                     help="also time the clustering-reuse step (P:1261-1262) and report amortised ms")
     ap.add_argument("--sel-flags", type=int, default=0,
-                    help="selection variants (NEXT-4): 1 = per-row counts (R11b), 2 = size-weighted (R9c)")
+                    help="selection variants (NEXT-4): 1 = per-row counts (R11b), 2 = size-weighted (R9c); "
+                         "256 = independent k-means partitioning (w/o On baseline, NEXT-2)")
     ap.add_argument("--parallel", choices=["head", "ulysses"], default=None,
                     help="multi-GPU split (default: ulysses for hunyuan_720p, head-parallel otherwise)")
     ap.add_argument("--cpu-sample-rows", type=int, default=1500,
@@ -239,9 +240,9 @@ def run_ours(args):
     # kept FLOPs of this rank's heads (state recomputed through the staged entries: same kernels,
     # same bits as inside the fused call)
     st = pb.coclust_assign(q_h, k_h, args.kq, args.kk, args.iters, seed=args.seed, ws=ws, head_offset=h0,
-                           heads_total=H_total)
+                           heads_total=H_total, kmeans=bool(args.sel_flags & pb.CLUSTER_KMEANS))
     sel = pb.block_select(st["cq"], st["ck"], st["offs_q"], st["offs_k"], budget_all[h0:h1].contiguous(),
-                          args.tau, args.theta, rule, ws=ws, flags=args.sel_flags if mode == "head" else 0)
+                          args.tau, args.theta, rule, ws=ws, flags=(args.sel_flags & 3) if mode == "head" else 0)
     n_keep, kept = sel[0], sel[1]
     torch.cuda.synchronize()
     oq = st["offs_q"].cpu().numpy().reshape(B * H, -1)
@@ -402,7 +403,7 @@ def run_ours(args):
                      "traffic": traffic,
                      "algorithmic": "kept FLOPs 4*d*sum_a |Q_a| sum_{c in kept[a]} |K_c| per launch (rank 0)"},
         "layer_kept_tflops": f_kept_total / (ms * 1e-3) / 1e12,
-        "gpu_launches": pb.launches_per_layer(args.iters) * K,
+        "gpu_launches": pb.launches_per_layer(args.iters, bool(args.sel_flags & pb.CLUSTER_KMEANS)) * K,
         "clocks": clk, "e2e": e2e, "cpu_baseline": cpu, "clustering_reuse": reuse,
     }
     print(json.dumps(line), flush=True)

@@ -100,6 +100,23 @@ cs_status coclust_assign_step(int B, int H, int N, int d, cs_bf16_in x, int ka,
                               const float* c_anchor, int ks, const float* c_self,
                               int32_t* labels, void* ws, size_t ws_bytes, void* stream);
 
+/* Independent k-means baseline (the "w/o On" ablation; SVG2's K-means partitioning,
+ * P:1270-1273).  Same arguments, outputs and sampler (R4) as coclust_assign, but
+ * each side is clustered alone by Lloyd's algorithm in raw token space: L(i) = argmin_j
+ * ||x_i - c_j||_2 (ties -> lowest j), then C_j = member mean (empty keeps its row, R5); keys
+ * first, then queries, iters times.  Computed by the assignment GEMM with W_j = c_j (bf16 hi + lo)
+ * and a -||c_j||^2/2 bias in the argmax epilogue. */
+cs_status kmeans_assign(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in k, int kq, int kk,
+                        int iters, uint64_t seed, int head_offset, int heads_total,
+                        const int32_t* init_q, const int32_t* init_k, float* cq, float* ck,
+                        int32_t* lq, int32_t* lk, int32_t* perm_q, int32_t* offs_q, int32_t* perm_k,
+                        int32_t* offs_k, void* ws, size_t ws_bytes, void* stream);
+
+/* One k-means assignment with given centroids c_self [B,H,ks,d] fp32 -> labels [B,H,N] (parity
+ * helper, as coclust_assign_step). */
+cs_status kmeans_assign_step(int B, int H, int N, int d, cs_bf16_in x, int ks, const float* c_self,
+                             int32_t* labels, void* ws, size_t ws_bytes, void* stream);
+
 /* Centroid update "C <- Mean(X via L)": c_inout [B,H,k,d] fp32; rows of empty clusters
  * are left unchanged (R5).  perm/offs as produced by coclust_permute.  If x_perm is non-NULL it
  * also receives the cluster-sorted copy x_perm[bh][p][:] = x[b,h,perm[bh][p],:] (bf16,
@@ -135,7 +152,10 @@ enum {
   /* R9c: block importance z_ac = Abar_ac / sqrt(d) + log|K_c| (softmax mass of a key block =
    * the mass its |K_c| tokens would get at the centroid logit); ranking and Recall both use z
    * (descending, ties -> lower index). */
-  CS_SEL_SIZE_WEIGHTED = 2
+  CS_SEL_SIZE_WEIGHTED = 2,
+  /* Fused entries only: partition Q and K by the independent k-means baseline (kmeans_assign)
+   * instead of Alg. 1 co-clustering — the paper's "w/o On" ablation, SVG2-style. */
+  CS_CLUSTER_KMEANS = 0x100
 };
 
 /* block_select with selection flags.  n_keep [B,H] always receives the shared count (R11);
@@ -178,7 +198,8 @@ cs_status coclust_sparse_attention(int B, int H, int N, int d, cs_bf16_in q, cs_
                                    float scale, cs_bf16_out o, void* ws, size_t ws_bytes,
                                    void* stream, void* const* stage_events);
 
-/* coclust_sparse_attention with selection flags (CS_SEL_*); sel_flags = 0 is the base entry. */
+/* coclust_sparse_attention with flags (CS_SEL_* selection variants, CS_CLUSTER_KMEANS baseline
+ * partitioning); sel_flags = 0 is the base entry. */
 cs_status coclust_sparse_attention_ex(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in k,
                                       cs_bf16_in v, int kq, int kk, int iters, uint64_t seed,
                                       int head_offset, int heads_total, const float* budget,

@@ -20,6 +20,7 @@ __all__ = [
 
 RULE_DENSITY, RULE_AS_WRITTEN, RULE_FIXED = 0, 1, 2
 SEL_PER_ROW, SEL_SIZE_WEIGHTED = 1, 2  # block_select_ex flags (include/coclust.h, NEXT-4)
+CLUSTER_KMEANS = 0x100                 # fused entries: independent k-means partitioning (NEXT-2)
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("COCLUST_LIB", os.path.join(_HERE, "libcoclust.so"))
 
@@ -51,6 +52,9 @@ _SIG = {
     "coclust_assign": (_I, [_I, _I, _I, _I, _BF16In, _BF16In, _I, _I, _I, ctypes.c_uint64, _I, _I, _P, _P,
                             _P, _P, _P, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P]),
     "coclust_assign_step": (_I, [_I, _I, _I, _I, _BF16In, _I, _P, _I, _P, _P, _P, ctypes.c_size_t, _P]),
+    "kmeans_assign": (_I, [_I, _I, _I, _I, _BF16In, _BF16In, _I, _I, _I, ctypes.c_uint64, _I, _I, _P, _P,
+                           _P, _P, _P, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P]),
+    "kmeans_assign_step": (_I, [_I, _I, _I, _I, _BF16In, _I, _P, _P, _P, ctypes.c_size_t, _P]),
     "coclust_update_centroids": (_I, [_I, _I, _I, _I, _BF16In, _I, _P, _P, _P, _P, _P]),
     "coclust_permute": (_I, [_I, _I, _I, _P, _P, _P, _P, ctypes.c_size_t, _P]),
     "block_select": (_I, [_I, _I, _I, _I, _I, _P, _P, _P, _P, _P, ctypes.c_double, ctypes.c_double,
@@ -118,11 +122,11 @@ def _cuda(t: torch.Tensor, name: str):
         raise ValueError(f"{name} must be a CUDA tensor (no CPU fallback)")
 
 
-def launches_per_layer(iters: int) -> int:
+def launches_per_layer(iters: int, kmeans: bool = False) -> int:
     """Kernels the fused entry launches per layer: init_sample 1; per iteration and side: anchor
-    prep 2 + assign GEMM 1 + counting sort 3 + centroid update 1; selection 4 (Abar, rows,
-    count, emit); V permute 1; work list 1; attention 1."""
-    return 1 + iters * 2 * 7 + 4 + 1 + 1 + 1
+    prep 2 (k-means: 1) + assign GEMM 1 + counting sort 3 + centroid update 1; selection 4 (Abar,
+    rows, count, emit); V permute 1; work list 1; attention 1."""
+    return 1 + iters * 2 * (6 if kmeans else 7) + 4 + 1 + 1 + 1
 
 
 def workspace_bytes(B, H, N, d, kq, kk) -> int:
@@ -150,8 +154,9 @@ def _ws(ws, nbytes, device):
 
 
 def coclust_assign(q, k, kq, kk, iters, seed=0, init_q=None, init_k=None, ws=None,
-                   head_offset=0, heads_total=0):
-    """Algorithm 1 for every (b,h) + final permutation.  Returns a dict of device tensors."""
+                   head_offset=0, heads_total=0, kmeans=False):
+    """Algorithm 1 for every (b,h) + final permutation.  Returns a dict of device tensors.
+    kmeans=True: the independent k-means baseline (kmeans_assign, NEXT-2) with the same outputs."""
     _cuda(q, "q")
     B, H, N, d = q.shape
     dev = q.device
@@ -162,7 +167,7 @@ def coclust_assign(q, k, kq, kk, iters, seed=0, init_q=None, init_k=None, ws=Non
              perm_q=torch.empty(B, H, N, **i32), offs_q=torch.empty(B, H, kq + 1, **i32),
              perm_k=torch.empty(B, H, N, **i32), offs_k=torch.empty(B, H, kk + 1, **i32))
     w, wn = _ws(ws, workspace_bytes(B, H, N, d, kq, kk), dev)
-    _check(lib().coclust_assign(B, H, N, d, _bf16(q), _bf16(k), kq, kk, iters, seed, head_offset,
+    _check((lib().kmeans_assign if kmeans else lib().coclust_assign)(B, H, N, d, _bf16(q), _bf16(k), kq, kk, iters, seed, head_offset,
                                 heads_total, _ptr(init_q),
                                 _ptr(init_k), _ptr(r["cq"]), _ptr(r["ck"]), _ptr(r["lq"]),
                                 _ptr(r["lk"]), _ptr(r["perm_q"]), _ptr(r["offs_q"]),
@@ -179,6 +184,18 @@ def coclust_assign_step(x, c_anchor, c_self, ws=None, labels=None):
     w, wn = _ws(ws, workspace_bytes(B, H, N, d, ka, ks), x.device)
     _check(lib().coclust_assign_step(B, H, N, d, _bf16(x), ka, _ptr(c_anchor.contiguous()), ks,
                                      _ptr(c_self.contiguous()), _ptr(labels), w, wn, _stream(x)))
+    return labels
+
+
+def kmeans_assign_step(x, c_self, ws=None, labels=None):
+    """One k-means assignment (NEXT-2): labels [B,H,N] int32 = argmin_j ||x_i - c_j||."""
+    _cuda(x, "x")
+    B, H, N, d = x.shape
+    ks = c_self.shape[2]
+    labels = torch.empty(B, H, N, dtype=torch.int32, device=x.device) if labels is None else labels
+    w, wn = _ws(ws, workspace_bytes(B, H, N, d, ks, ks), x.device)
+    _check(lib().kmeans_assign_step(B, H, N, d, _bf16(x), ks, _ptr(c_self.contiguous()), _ptr(labels), w, wn,
+                                    _stream(x)))
     return labels
 
 

@@ -63,6 +63,7 @@ struct AssignScratch {
   double* gamma;
   __nv_bfloat16* wsplit;
   int32_t* hist;
+  float* bias;  // k-means baseline: -||c_j||^2 / 2 per (bh, padded centroid)
 };
 AssignScratch carve_assign(Carve& c, int BH, int N, int d, int kq, int kk) {
   AssignScratch s;
@@ -70,6 +71,7 @@ AssignScratch carve_assign(Carve& c, int BH, int N, int d, int kq, int kk) {
   s.gamma = c.take<double>((size_t)BH * d * d);
   s.wsplit = c.take<__nv_bfloat16>((size_t)BH * std::max(pad_k(kq), pad_k(kk)) * 2 * d);
   s.hist = c.take<int32_t>((size_t)BH * ((N + kSortTile - 1) / kSortTile) * kmax);
+  s.bias = c.take<float>((size_t)BH * std::max(pad_k(kq), pad_k(kk)));
   return s;
 }
 struct SelectScratch {
@@ -228,7 +230,20 @@ cs_status run_assign_step(int B, int H, int N, int d, cs_bf16_in x, int ka, cons
   CUtensorMap tx, tw;
   CS_CHECK(make_map_x(&tx, x, B, H, N, d));
   CS_CHECK(make_map_2d(&tw, sc.wsplit, (uint64_t)BH * ks_pad, 2 * d, nch));
-  CS_CUDA(launch_assign_gemm(&tx, &tw, B, H, N, d, ks, nch, ks_pad, labels, st), "assign_gemm");
+  CS_CUDA(launch_assign_gemm(&tx, &tw, B, H, N, d, ks, nch, ks_pad, nullptr, labels, st), "assign_gemm");
+  return CS_OK;
+}
+
+// k-means baseline half-step (NEXT-2): L(i) = argmin_j ||x_i - c_j|| through the same GEMM
+cs_status run_kmeans_step(int B, int H, int N, int d, cs_bf16_in x, int ks, const float* cself, int32_t* labels,
+                          const AssignScratch& sc, cudaStream_t st) {
+  const int BH = B * H;
+  const int nch = chunk_n(ks), ks_pad = pad_k(ks);
+  CS_CUDA(launch_kmeans_prep(cself, ks, ks_pad, BH, d, sc.wsplit, sc.bias, st), "kmeans_prep");
+  CUtensorMap tx, tw;
+  CS_CHECK(make_map_x(&tx, x, B, H, N, d));
+  CS_CHECK(make_map_2d(&tw, sc.wsplit, (uint64_t)BH * ks_pad, 2 * d, nch));
+  CS_CUDA(launch_assign_gemm(&tx, &tw, B, H, N, d, ks, nch, ks_pad, sc.bias, labels, st), "assign_gemm");
   return CS_OK;
 }
 
@@ -236,18 +251,20 @@ cs_status run_assign(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in k, int
                      uint64_t seed, int h_off, int h_tot, const int32_t* init_q, const int32_t* init_k, float* cq, float* ck,
                      int32_t* lq, int32_t* lk, int32_t* perm_q, int32_t* offs_q, int32_t* perm_k,
                      int32_t* offs_k, const AssignScratch& sc, __nv_bfloat16* qp_out,
-                     __nv_bfloat16* kp_out, cudaStream_t st) {
+                     __nv_bfloat16* kp_out, cudaStream_t st, bool kmeans = false) {
   const int BH = B * H;
   const XView xq = view(q, H), xk = view(k, H);
   CS_CUDA(launch_init_sample(xq, xk, BH, N, d, kq, kk, seed, h_off, h_tot, init_q, init_k, cq, ck, st), "init_sample");
   for (int it = 0; it < iters; ++it) {
     const bool last = it == iters - 1;
-    // Step A: query-aware key-side partitioning
-    CS_CHECK(run_assign_step(B, H, N, d, k, kq, cq, kk, ck, lk, sc, st));
+    // Step A: query-aware key-side partitioning; k-means baseline: keys alone
+    if (kmeans) CS_CHECK(run_kmeans_step(B, H, N, d, k, kk, ck, lk, sc, st));
+    else CS_CHECK(run_assign_step(B, H, N, d, k, kq, cq, kk, ck, lk, sc, st));
     CS_CUDA(launch_csort(lk, BH, N, kk, perm_k, offs_k, sc.hist, st), "csort_k");
     CS_CUDA(launch_seg_mean(xk, BH, N, d, kk, perm_k, offs_k, ck, last ? kp_out : nullptr, st), "seg_mean_k");
-    // Step B: key-aware query-side partitioning
-    CS_CHECK(run_assign_step(B, H, N, d, q, kk, ck, kq, cq, lq, sc, st));
+    // Step B: key-aware query-side partitioning; k-means baseline: queries alone
+    if (kmeans) CS_CHECK(run_kmeans_step(B, H, N, d, q, kq, cq, lq, sc, st));
+    else CS_CHECK(run_assign_step(B, H, N, d, q, kk, ck, kq, cq, lq, sc, st));
     CS_CUDA(launch_csort(lq, BH, N, kq, perm_q, offs_q, sc.hist, st), "csort_q");
     CS_CUDA(launch_seg_mean(xq, BH, N, d, kq, perm_q, offs_q, cq, last ? qp_out : nullptr, st), "seg_mean_q");
   }
@@ -313,7 +330,7 @@ cs_status check_heads(int H, int& h_off, int& h_tot) {
   return CS_OK;
 }
 
-cs_status coclust_assign(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in k, int kq, int kk, int iters,
+static cs_status assign_entry(bool kmeans, int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in k, int kq, int kk, int iters,
                          uint64_t seed, int head_offset, int heads_total, const int32_t* init_q, const int32_t* init_k, float* cq, float* ck,
                          int32_t* lq, int32_t* lk, int32_t* perm_q, int32_t* offs_q, int32_t* perm_k,
                          int32_t* offs_k, void* ws, size_t ws_bytes, void* stream) {
@@ -332,7 +349,37 @@ cs_status coclust_assign(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in k,
   Carve c(ws);
   AssignScratch sc = carve_assign(c, BH, N, d, kq, kk);
   return run_assign(B, H, N, d, q, k, kq, kk, iters, seed, head_offset, heads_total, init_q, init_k, cq, ck, lq, lk, perm_q, offs_q,
-                    perm_k, offs_k, sc, nullptr, nullptr, static_cast<cudaStream_t>(stream));
+                    perm_k, offs_k, sc, nullptr, nullptr, static_cast<cudaStream_t>(stream), kmeans);
+}
+
+cs_status coclust_assign(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in k, int kq, int kk, int iters,
+                         uint64_t seed, int head_offset, int heads_total, const int32_t* init_q, const int32_t* init_k,
+                         float* cq, float* ck, int32_t* lq, int32_t* lk, int32_t* perm_q, int32_t* offs_q,
+                         int32_t* perm_k, int32_t* offs_k, void* ws, size_t ws_bytes, void* stream) {
+  return assign_entry(false, B, H, N, d, q, k, kq, kk, iters, seed, head_offset, heads_total, init_q, init_k, cq, ck,
+                      lq, lk, perm_q, offs_q, perm_k, offs_k, ws, ws_bytes, stream);
+}
+
+cs_status kmeans_assign(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in k, int kq, int kk, int iters,
+                        uint64_t seed, int head_offset, int heads_total, const int32_t* init_q, const int32_t* init_k,
+                        float* cq, float* ck, int32_t* lq, int32_t* lk, int32_t* perm_q, int32_t* offs_q,
+                        int32_t* perm_k, int32_t* offs_k, void* ws, size_t ws_bytes, void* stream) {
+  return assign_entry(true, B, H, N, d, q, k, kq, kk, iters, seed, head_offset, heads_total, init_q, init_k, cq, ck,
+                      lq, lk, perm_q, offs_q, perm_k, offs_k, ws, ws_bytes, stream);
+}
+
+cs_status kmeans_assign_step(int B, int H, int N, int d, cs_bf16_in x, int ks, const float* c_self, int32_t* labels,
+                             void* ws, size_t ws_bytes, void* stream) {
+  g_err[0] = 0;
+  CS_CHECK(check_dims(B, H, N, d));
+  if (ks < 1 || ks > kMaxClusters) return fail(CS_ERR_ARG, "ks must be in [1, %d] (got %d)", kMaxClusters, ks);
+  CS_CHECK(check_bf16(x.ptr, x.sb, x.sh, x.sn, "x"));
+  NEED(c_self, "c_self"); NEED(labels, "labels");
+  const int BH = B * H;
+  CS_CHECK(check_ws(ws, ws_bytes, need_assign(BH, N, d, ks, ks)));
+  Carve c(ws);
+  AssignScratch sc = carve_assign(c, BH, N, d, ks, ks);
+  return run_kmeans_step(B, H, N, d, x, ks, c_self, labels, sc, static_cast<cudaStream_t>(stream));
 }
 
 cs_status coclust_assign_step(int B, int H, int N, int d, cs_bf16_in x, int ka, const float* c_anchor, int ks,
@@ -461,8 +508,8 @@ cs_status check_layer_args(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in 
   if (!(tau > 0.0 && tau <= 1.0)) return fail(CS_ERR_ARG, "tau must be in (0, 1] (got %g)", tau);
   if (!(theta > 0.0 && theta < 1.0)) return fail(CS_ERR_ARG, "theta must be in (0, 1) (got %g)", theta);
   if (rule < 0 || rule > 2) return fail(CS_ERR_ARG, "unknown rule %d", rule);
-  if (sel_flags & ~(CS_SEL_PER_ROW | CS_SEL_SIZE_WEIGHTED))
-    return fail(CS_ERR_ARG, "unknown selection flags 0x%x", sel_flags);
+  if (sel_flags & ~(CS_SEL_PER_ROW | CS_SEL_SIZE_WEIGHTED | CS_CLUSTER_KMEANS))
+    return fail(CS_ERR_ARG, "unknown flags 0x%x", sel_flags);
   if (!(scale > 0.f)) return fail(CS_ERR_ARG, "scale must be > 0 (got %g)", (double)scale);
   CS_CHECK(check_heads(H, head_offset, heads_total));
   CS_CHECK(check_bf16(q.ptr, q.sb, q.sh, q.sn, "q"));
@@ -484,10 +531,12 @@ cs_status run_layer(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in k, cs_b
   SelectScratch se = carve_select(c, BH, kq, kk);
   if (recompute) {
     CS_CHECK(run_assign(B, H, N, d, q, k, kq, kk, iters, seed, head_offset, heads_total, nullptr, nullptr, s.cq,
-                        s.ck, s.lq, s.lk, s.perm_q, s.offs_q, s.perm_k, s.offs_k, as, at.qp, at.kp, st));
+                        s.ck, s.lq, s.lk, s.perm_q, s.offs_q, s.perm_k, s.offs_k, as, at.qp, at.kp, st,
+                        (sel_flags & CS_CLUSTER_KMEANS) != 0));
     if (ev) CS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(ev[0]), st), "event");
     CS_CUDA(launch_block_select(BH, H, kq, kk, d, s.cq, s.ck, s.offs_q, s.offs_k, budget, tau, theta, rule,
-                                sel_flags, s.n_keep, s.n_rows, s.kept, se.order, se.cnt, se.abar, st),
+                                sel_flags & (CS_SEL_PER_ROW | CS_SEL_SIZE_WEIGHTED), s.n_keep, s.n_rows, s.kept,
+                                se.order, se.cnt, se.abar, st),
             "block_select");
     if (ev) CS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(ev[1]), st), "event");
   } else {

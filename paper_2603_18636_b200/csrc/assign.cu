@@ -13,6 +13,8 @@
 // double-buffered across units.
 // Warps 0-3: epilogue tile 0, 4-7: epilogue tile 1 (thread = token row = TMEM lane),
 // warp 8: TMA producer, warp 9: TMEM allocator + MMA issuer.
+// With a bias (the k-means baseline, NEXT-2: W_j = c_j, bias_j = -||c_j||^2 / 2, so argmax_j
+// x.c_j - ||c_j||^2/2 = argmin_j ||x - c_j||) the epilogue adds bias[bh][j] before the argmax.
 #include "kernels.cuh"
 
 namespace cs {
@@ -37,11 +39,11 @@ struct Smem {
   static constexpr int ALLOC = BYTES + 1024;
 };
 
-template <int D>
+template <int D, bool BIAS>
 __global__ void __launch_bounds__(NTHREADS, 1)
     k_assign(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_w,
              int H, int N, int ks, int nch, int ks_pad, int units_per_head, int num_units,
-             int32_t* __restrict__ labels) {
+             const float* __restrict__ bias, int32_t* __restrict__ labels) {
   using L = Smem<D>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -160,11 +162,21 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         for (int c0 = 0; c0 < nch; c0 += 16) {
           uint32_t v[16];
           tmem_ld16(t_acc + c0, v);
+          float bs[16];
+          if constexpr (BIAS) {  // warp-uniform address: broadcast loads
+            const float4* b4 = reinterpret_cast<const float4*>(bias + (size_t)bh * ks_pad + jbase + c0);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float4 q = __ldg(b4 + i);
+              bs[4 * i] = q.x; bs[4 * i + 1] = q.y; bs[4 * i + 2] = q.z; bs[4 * i + 3] = q.w;
+            }
+          }
           tmem_wait_ld();
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             const int j = jbase + c0 + i;
-            const float x = __uint_as_float(v[i]);
+            float x = __uint_as_float(v[i]);
+            if constexpr (BIAS) x += bs[i];
             if (j < ks && x > best) { best = x; best_j = j; }
           }
         }
@@ -188,7 +200,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 int assign_chunk_n(int ks) { return ks <= asg::NCH_MAX ? (ks + 15) / 16 * 16 : asg::NCH_MAX; }
 
 cudaError_t launch_assign_gemm(const CUtensorMap* tm_x, const CUtensorMap* tm_w, int B, int H, int N,
-                               int d, int ks, int nch, int ks_pad, int32_t* labels, cudaStream_t st) {
+                               int d, int ks, int nch, int ks_pad, const float* bias, int32_t* labels,
+                               cudaStream_t st) {
   static int num_sms = 0;
   if (!num_sms) {
     int dev = 0;
@@ -199,19 +212,19 @@ cudaError_t launch_assign_gemm(const CUtensorMap* tm_x, const CUtensorMap* tm_w,
   const int units_per_head = (N + asg::TILES * asg::BM - 1) / (asg::TILES * asg::BM);
   const int num_units = units_per_head * B * H;
   const int grid = num_units < num_sms ? num_units : num_sms;
-  if (d == 128) {
-    auto kfn = asg::k_assign<128>;
-    const int smem = asg::Smem<128>::ALLOC;
+  auto launch = [&](auto kfn, int smem) -> cudaError_t {
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    kfn<<<grid, asg::NTHREADS, smem, st>>>(*tm_x, *tm_w, H, N, ks, nch, ks_pad, units_per_head, num_units, labels);
-  } else {
-    auto kfn = asg::k_assign<64>;
-    const int smem = asg::Smem<64>::ALLOC;
-    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    kfn<<<grid, asg::NTHREADS, smem, st>>>(*tm_x, *tm_w, H, N, ks, nch, ks_pad, units_per_head, num_units, labels);
-  }
+    kfn<<<grid, asg::NTHREADS, smem, st>>>(*tm_x, *tm_w, H, N, ks, nch, ks_pad, units_per_head, num_units, bias,
+                                           labels);
+    return cudaSuccess;
+  };
+  cudaError_t e;
+  if (d == 128)
+    e = bias ? launch(asg::k_assign<128, true>, asg::Smem<128>::ALLOC) : launch(asg::k_assign<128, false>, asg::Smem<128>::ALLOC);
+  else
+    e = bias ? launch(asg::k_assign<64, true>, asg::Smem<64>::ALLOC) : launch(asg::k_assign<64, false>, asg::Smem<64>::ALLOC);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

@@ -253,6 +253,43 @@ __global__ void __launch_bounds__(256) k_anchor_w(const float* __restrict__ cs_,
 }
 
 // ---------------------------------------------------------------------------------------------
+// k-means baseline (NEXT-2, "w/o On" P:1058): L(i) = argmin_j ||x_i - c_j|| = argmax_j x_i.c_j -
+// ||c_j||^2/2 -> the same assignment GEMM with W_j = c_j (bf16 hi + lo) and a bias epilogue.
+// grid (ks_pad / 8, BH), block 256: one warp per centroid.
+// ---------------------------------------------------------------------------------------------
+template <int D>
+__global__ void __launch_bounds__(256) k_kmeans_w(const float* __restrict__ cs_, int ks, int ks_pad,
+                                                  __nv_bfloat16* __restrict__ wsplit, float* __restrict__ bias) {
+  constexpr int PL = D / 32;  // columns per lane
+  const int bh = blockIdx.y, j = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (j >= ks_pad) return;
+  __nv_bfloat16* out = wsplit + ((size_t)bh * ks_pad + j) * (2 * D);
+  double n2 = 0.0;
+#pragma unroll
+  for (int i = 0; i < PL; ++i) {
+    const int e = lane + 32 * i;
+    const float c = j < ks ? cs_[((size_t)bh * ks + j) * D + e] : 0.f;
+    const __nv_bfloat16 hi = __float2bfloat16(c);
+    out[e] = hi;
+    out[D + e] = __float2bfloat16(c - __bfloat162float(hi));
+    n2 = fma((double)c, (double)c, n2);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) n2 += __shfl_xor_sync(0xffffffffu, n2, o);
+  if (lane == 0) bias[(size_t)bh * ks_pad + j] = j < ks ? (float)(-0.5 * n2) : 0.f;
+}
+
+cudaError_t launch_kmeans_prep(const float* cself, int ks, int ks_pad, int BH, int d, __nv_bfloat16* wsplit,
+                               float* bias, cudaStream_t st) {
+  const dim3 grid((ks_pad + 7) / 8, BH);
+  if (d == 128)
+    k_kmeans_w<128><<<grid, 256, 0, st>>>(cself, ks, ks_pad, wsplit, bias);
+  else
+    k_kmeans_w<64><<<grid, 256, 0, st>>>(cself, ks, ks_pad, wsplit, bias);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------------
 // a5/a7: centroid update.  grid (ceil(K / CPB), BH), block 256 (8 warps), CPB = 8 / NWC clusters
 // per CTA with NWC warps each (NWC from the mean cluster size, so small clusters do not leave
 // most of a CTA idle).  Warp ws of a cluster sums a contiguous chunk of its sorted positions;

@@ -30,6 +30,9 @@ cudaError_t launch_init_sample(XView q, XView k, int BH, int N, int d, int kq, i
                                const int32_t* init_k, float* cq, float* ck, cudaStream_t st);
 cudaError_t launch_anchor_prep(const float* ca, int ka, const float* cself, int ks, int ks_pad,
                                int BH, int d, double* gamma, __nv_bfloat16* wsplit, cudaStream_t st);
+// k-means baseline (NEXT-2): Wsplit[bh][j] = [bf16(c_j) | bf16(c_j - bf16(c_j))], bias = -||c_j||^2 / 2
+cudaError_t launch_kmeans_prep(const float* cself, int ks, int ks_pad, int BH, int d, __nv_bfloat16* wsplit,
+                               float* bias, cudaStream_t st);
 cudaError_t launch_seg_mean(XView x, int BH, int N, int d, int K, const int32_t* perm,
                             const int32_t* offs, float* C, __nv_bfloat16* xperm, cudaStream_t st);
 cudaError_t launch_csort(const int32_t* lab, int BH, int N, int K, int32_t* perm, int32_t* offs,
@@ -43,7 +46,8 @@ cudaError_t launch_permute_rows(XView x, int BH, int N, int d, const int32_t* pe
 // box {64, nch}.
 int assign_chunk_n(int ks);  // centroid columns per TMEM chunk (UMMA N)
 cudaError_t launch_assign_gemm(const CUtensorMap* tm_x, const CUtensorMap* tm_w, int B, int H, int N,
-                               int d, int ks, int nch, int ks_pad, int32_t* labels, cudaStream_t st);
+                               int d, int ks, int nch, int ks_pad, const float* bias, int32_t* labels,
+                               cudaStream_t st);
 
 // ---- select.cu
 cudaError_t launch_block_select(int BH, int H, int kq, int kk, int d, const float* cq,

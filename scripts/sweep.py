@@ -42,16 +42,16 @@ def peaks():
 
 def kept_flops(q, k, kq, kk, iters, budget, tau, theta, rule, seed, ws, flags=0):
     """F_kept of one layer, from the staged entries (same kernels and bits as the fused call)."""
-    st = pb.coclust_assign(q, k, kq, kk, iters, seed=seed, ws=ws)
+    st = pb.coclust_assign(q, k, kq, kk, iters, seed=seed, ws=ws, kmeans=bool(flags & pb.CLUSTER_KMEANS))
     sel = pb.block_select(st["cq"], st["ck"], st["offs_q"], st["offs_k"], budget, tau, theta, rule, ws=ws,
-                          flags=flags)
+                          flags=flags & 3)
     n_keep, kept = sel[0], sel[1]
     B, H, N, d = q.shape
     oq = st["offs_q"].cpu().numpy().reshape(B * H, -1)
     ok = st["offs_k"].cpu().numpy().reshape(B * H, -1)
     kp = kept.cpu().numpy().reshape(B * H, kq, kk)
     nk = n_keep.cpu().numpy().reshape(-1)
-    nrows = sel[2].cpu().numpy().reshape(B * H, kq) if flags else np.repeat(nk[:, None], kq, 1)
+    nrows = sel[2].cpu().numpy().reshape(B * H, kq) if flags & 3 else np.repeat(nk[:, None], kq, 1)
     f = 0
     for bh in range(B * H):
         sq, sk = np.diff(oq[bh]), np.diff(ok[bh])

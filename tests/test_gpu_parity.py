@@ -481,3 +481,53 @@ def test_clustering_reuse_cached_entry(pb):
                                       st.lk[0, h].cpu().numpy(), st.kept[0, h, :, :n].cpu().numpy())
         err = np.abs(f64(o2[0, h]) - ref_o)
         assert err.max() <= ATOL_MAX and err.mean() <= ATOL_MEAN
+
+
+# ------------------------------------------------------------------------- NEXT-2 k-means baseline
+@pytest.mark.parametrize("d,N,ks", [(64, 2048, 16), (128, 8192, 500), (128, 3000, 100), (128, 4096, 1024),
+                                    (64, 1000, 1)])
+def test_kmeans_assign_step(pb, d, N, ks):
+    """k-means half-step through the assignment GEMM with the -||c||^2/2 bias epilogue: labels
+    identical to the oracle's argmin_j ||x_i - c_j|| outside the near-tie band (P1 rule)."""
+    w = video_qkv(4, 16, max(1, N // 64), 2, d, seed=ks + 3)
+    g = torch.Generator().manual_seed(ks)
+    C = torch.randn(1, 2, ks, d, generator=g) * 0.8
+    for X in (w.q, w.k):
+        lab = pb.kmeans_assign_step(X.cuda(), C.cuda()).cpu()
+        for h in range(2):
+            res = svoo.kmeans_step(f64(X[0, h]), C[0, h].double().numpy())
+            _check_labels(lab[0, h].numpy(), res, "kmeans")
+
+
+def test_kmeans_assign_chain_teacher_forced_and_layer(pb):
+    """Every GPU k-means half-step matches the oracle given the oracle's centroids; the whole
+    "w/o On" layer (CLUSTER_KMEANS) equals the staged entries bit for bit and the oracle within P5."""
+    w = video_qkv(8, 16, 24, 1, 128, seed=9)
+    Q, K = f64(w.q[0, 0]), f64(w.k[0, 0])
+    cc = svoo.cocluster_kmeans(Q, K, 40, 120, 2, seed=0)
+    for t in cc.trace:
+        X = w.k if t["side"] == "k" else w.q
+        cs = torch.from_numpy(t["C_self"]).float()[None, None].cuda()
+        lab = pb.kmeans_assign_step(X.cuda(), cs)[0, 0].cpu().numpy()
+        ok = t["gap"] >= GAP_TOL
+        assert np.sum((lab != t["labels"]) & ok) == 0
+    q, k, v = w.q.cuda(), w.k.cuda(), w.v.cuda()
+    budget = torch.tensor([0.3], dtype=torch.float32).cuda()
+    st = pb.coclust_assign(q, k, 40, 120, 2, seed=0, kmeans=True)
+    n_keep, kept = pb.block_select(st["cq"], st["ck"], st["offs_q"], st["offs_k"], budget, 0.95, 0.1,
+                                   pb.RULE_DENSITY)
+    o = pb.block_sparse_attn(q, k, v, st["perm_q"], st["offs_q"], st["perm_k"], st["offs_k"], n_keep, kept)
+    of = pb.coclust_sparse_attention(q, k, v, 40, 120, 2, budget, seed=0, sel_flags=pb.CLUSTER_KMEANS)
+    torch.cuda.synchronize()
+    assert torch.equal(o, of)
+    n = int(n_keep[0, 0])
+    ref = svoo.sparse_attention(Q, K, f64(w.v[0, 0]), st["lq"][0, 0].cpu().numpy(), st["lk"][0, 0].cpu().numpy(),
+                                kept[0, 0, :, :n].cpu().numpy())
+    err = np.abs(f64(o[0, 0]) - ref)
+    assert err.max() <= ATOL_MAX and err.mean() <= ATOL_MEAN
+    # every nonempty centroid is the mean of its members (P2 on the k-means side)
+    for side, X, L, C in (("k", K, st["lk"], st["ck"]), ("q", Q, st["lq"], st["cq"])):
+        Lh, Ch = L[0, 0].cpu().numpy(), C[0, 0].cpu().double().numpy()
+        for j in np.unique(Lh):
+            m = X[Lh == j].mean(0)
+            assert np.allclose(Ch[j], m, rtol=1e-5, atol=1e-5), side
