@@ -32,6 +32,9 @@ Functions and their pins (tests/test_oracle_*.py):
                                                           Lloyd objective non-increasing
   reference_pairs / block_pair_* (recall)   P:181-183     pinned: brute-force minimal prefix,
                                                           identity / single-block partitions
+  attention_density / sparsity_schedule     P:1176-1191   pinned: uniform / one-hot / geometric
+                                                          rows (closed forms), brute-force minimal
+                                                          subsets, scipy norm.ppf(0.95)
 """
 from __future__ import annotations
 
@@ -512,3 +515,46 @@ def pairs_to_cover(cnt: np.ndarray, frac: float = 1.0) -> int:
     flat = np.sort(cnt.ravel())[::-1]
     cs = np.cumsum(flat)
     return int(np.searchsorted(cs, frac * cs[-1] - 1e-9, side="left")) + 1
+
+
+# ----------------------------------------------------------------------------------------------
+# Offline layer-wise sparsity profiling
+# ----------------------------------------------------------------------------------------------
+def attention_density(A: np.ndarray, tau: float = 0.95) -> tuple[float, np.ndarray]:
+    """for each row i of the post-softmax attention A (n x n), S(i) = the minimal
+    descending prefix with sum >= tau ("reaches tau" with the R9b tolerance 1e-12);
+    d = (1/n) sum_i |S(i)| / n.  Returns (d, |S(i)| per row)."""
+    A = np.asarray(A, np.float64)
+    n = A.shape[1]
+    counts = np.empty(A.shape[0], dtype=np.int64)
+    for i in range(A.shape[0]):
+        cs = np.cumsum(np.sort(A[i])[::-1])
+        hit = np.nonzero(cs >= tau - RECALL_EPS)[0]
+        counts[i] = hit[0] + 1 if hit.size else n
+    return float(counts.sum()) / A.shape[0] / n, counts
+
+
+def attention_density_qk(Q: np.ndarray, K: np.ndarray, tau: float = 0.95, scale: float | None = None):
+    """attention_density of A = softmax(Q K^T * scale) (rows), fp64 (one head)."""
+    Q = np.asarray(Q, np.float64)
+    K = np.asarray(K, np.float64)
+    scale = 1.0 / math.sqrt(Q.shape[1]) if scale is None else scale
+    S = Q @ K.T * scale
+    S -= S.max(1, keepdims=True)
+    E = np.exp(S)
+    return attention_density(E / E.sum(1, keepdims=True), tau)
+
+
+Z_95 = 1.6448536269514722   # upper 0.95 quantile of N(0, 1) (P:1186, alpha = 0.95)
+
+
+def sparsity_schedule(d: np.ndarray, z: float = Z_95) -> dict:
+    """fit N(mu, sigma^2) to the m calibration densities of each (layer, head)
+    (axis 0 of d: [m, L, H]; maximum-likelihood sigma), d_hat = mu + z_alpha sigma, s = 1 - d_hat.
+    d_hat is clamped to 1 (R21: a density cannot exceed 1); it is the keep budget the DENSITY rule
+    consumes (R8)."""
+    d = np.asarray(d, np.float64)
+    mu = d.mean(axis=0)
+    sigma = d.std(axis=0, ddof=0)
+    d_hat = np.minimum(mu + z * sigma, 1.0)
+    return {"mu": mu, "sigma": sigma, "d_hat": d_hat, "s": 1.0 - d_hat}

@@ -482,3 +482,49 @@ def test_block_pair_recall_special_partitions():
     one = np.zeros(12, int)
     cnt1 = svoo.block_pair_counts(ref, one, one, 1, 1)
     assert cnt1[0, 0] == n and svoo.block_pair_recall(cnt1, 1) == 1.0 and svoo.pairs_to_cover(cnt1) == 1
+
+
+# ------------------------------------------------------------------ NEXT-3 offline profiler
+def test_density_closed_forms():
+    n = 40
+    U = np.full((3, n), 1.0 / n)                      # uniform rows: ceil(tau n) entries
+    for tau in (0.95, 0.5, 0.9, 1.0):
+        d, c = svoo.attention_density(U, tau)
+        assert np.all(c == math.ceil(tau * n - 1e-9)) and d == math.ceil(tau * n - 1e-9) / n
+    E = np.eye(n)                                     # one-hot rows: a single entry
+    d, c = svoo.attention_density(E, 0.95)
+    assert np.all(c == 1) and d == 1.0 / n
+    r = 0.7                                           # geometric row p_j ~ r^j (any column order)
+    g = r ** np.arange(n)
+    g /= g.sum()
+    perm = np.random.default_rng(0).permutation(n)
+    d, c = svoo.attention_density(g[perm][None], 0.95)
+    m = next(m for m in range(1, n + 1) if (1 - r ** m) / (1 - r ** n) >= 0.95)
+    assert c[0] == m
+
+
+def test_density_minimal_subset_bruteforce():
+    """The sorted prefix is the minimal subset reaching tau: check against all subsets (n = 7)."""
+    rng = np.random.default_rng(2)
+    for _ in range(5):
+        p = rng.dirichlet(np.ones(7) * 0.5)
+        best = min(len(sub) for k in range(1, 8) for sub in itertools.combinations(range(7), k)
+                   if p[list(sub)].sum() >= 0.8 - 1e-12)
+        assert svoo.attention_density(p[None], 0.8)[1][0] == best
+
+
+def test_density_qk_and_schedule():
+    rng = np.random.default_rng(4)
+    Q, K = rng.normal(size=(30, 16)), rng.normal(size=(30, 16))
+    d, c = svoo.attention_density_qk(Q, K, 0.95)
+    S = Q @ K.T / 4.0
+    A = np.exp(S - S.max(1, keepdims=True))
+    A /= A.sum(1, keepdims=True)
+    assert d == svoo.attention_density(A, 0.95)[0] and 0 < d <= 1
+    from scipy.stats import norm
+    assert abs(svoo.Z_95 - norm.ppf(0.95)) < 1e-12
+    dens = np.array([[[0.1, 0.5]], [[0.3, 0.7]]])     # m = 2 inputs, 1 layer, 2 heads
+    sch = svoo.sparsity_schedule(dens)
+    assert np.allclose(sch["mu"], [[0.2, 0.6]]) and np.allclose(sch["sigma"], [[0.1, 0.1]])
+    assert np.allclose(sch["d_hat"], [[0.2 + 0.1 * norm.ppf(0.95), min(1.0, 0.6 + 0.1 * norm.ppf(0.95))]])
+    assert np.allclose(sch["s"], 1 - sch["d_hat"])
