@@ -236,6 +236,21 @@ cs_status coclust_sparse_attention_cached(int B, int H, int N, int d, cs_bf16_in
                                           void* ws, size_t ws_bytes, void* stream,
                                           void* const* stage_events);
 
+/* Offline layer-wise sparsity profiling.  For every (b,h):
+ *   A = softmax(q k^T * scale) (rows), S(i) = the minimal descending prefix of row i whose mass
+ *   reaches tau (R9b tolerance 1e-12), counts[b][h][i] = |S(i)| (nullable [B,H,N] int32 out),
+ *   density[b][h] = (1/N) sum_i |S(i)| / N (double out [B,H]).
+ * No sort: after a row max / row sum pass, `passes` binning passes (0 -> 4) narrow the crossing of
+ * the descending cumulative mass to a log2-interval of width 65 / 32^passes; the count inside the
+ * final interval is interpolated from its elements' mean mass (exact unless several elements
+ * share that interval).  Each pass recomputes Q K^T on the tensor cores.  The Gaussian fit over
+ * calibration inputs and the schedule s = 1 - d_hat are host-side
+ * (paper_2603_18636_b200/profiler.py).  Workspace: cs_density_workspace_bytes(B, H, N). */
+size_t cs_density_workspace_bytes(int B, int H, int N);
+cs_status attention_density(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in k, double tau,
+                            float scale, int passes, int32_t* counts, double* density, void* ws,
+                            size_t ws_bytes, void* stream);
+
 /* Ulysses resharding helper (BASELINE configs[3]): dst[b][a] = src[a][b] for an
  * [A, B] grid of rows of row_bytes bytes (row_bytes a multiple of 16, pointers 16-byte aligned).
  * Packs a [N/P, H, d] token block into [P, N/P, H/P, d] per-destination chunks before the

@@ -72,6 +72,9 @@ _SIG = {
                                          ctypes.c_uint64, _I, _I, _P, ctypes.c_double, ctypes.c_double, _I,
                                          _I, ctypes.c_float, _BF16Out, _P, ctypes.c_size_t, _P, _P]),
     "cs_block_transpose": (_I, [_I, _I, ctypes.c_size_t, _P, _P, _P]),
+    "cs_density_workspace_bytes": (ctypes.c_size_t, [_I, _I, _I]),
+    "attention_density": (_I, [_I, _I, _I, _I, _BF16In, _BF16In, ctypes.c_double, ctypes.c_float, _I, _P, _P, _P,
+                               ctypes.c_size_t, _P]),
     "coclust_sparse_attention_cached": (_I, [_I, _I, _I, _I, _BF16In, _BF16In, _BF16In, _I, _I, _I,
                                              ctypes.c_uint64, _I, _I, _P, ctypes.c_double, ctypes.c_double,
                                              _I, _I, ctypes.c_float, _BF16Out, _P, _I, _P, ctypes.c_size_t,
@@ -292,6 +295,20 @@ def coclust_sparse_attention(q, k, v, kq, kk, iters, budget, *, seed=0, tau=0.95
                                           seed, head_offset, heads_total, _ptr(budget), float(tau), float(theta), int(rule),
                                           float(scale), _bf16(out, True), w, wn, _stream(q), evs))
     return out
+
+
+def attention_density(q, k, tau=0.95, scale=None, passes=0, counts=False, ws=None):
+    """Offline profiling (NEXT-3): attention density per (b,h) of softmax(q k^T scale)
+    at mass tau -> float64 [B,H] (and the per-row prefix sizes int32 [B,H,N] if counts)."""
+    _cuda(q, "q")
+    B, H, N, d = q.shape
+    scale = d ** -0.5 if scale is None else scale
+    dens = torch.empty(B, H, dtype=torch.float64, device=q.device)
+    cnt = torch.empty(B, H, N, dtype=torch.int32, device=q.device) if counts else None
+    w, wn = _ws(ws, int(lib().cs_density_workspace_bytes(B, H, N)), q.device)
+    _check(lib().attention_density(B, H, N, d, _bf16(q), _bf16(k), float(tau), float(scale), int(passes),
+                                   _ptr(cnt), _ptr(dens), w, wn, _stream(q)))
+    return (dens, cnt) if counts else dens
 
 
 def block_transpose(src, A, B, out=None):

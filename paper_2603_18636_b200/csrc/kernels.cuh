@@ -72,4 +72,9 @@ cudaError_t launch_bsa_fwd(const CUtensorMap* tm_q, const KVMaps* kv,
                            float scale, __nv_bfloat16* o, long long osb, long long osh,
                            long long osn, cudaStream_t st);
 
+// ---- profile.cu : offline attention density (NEXT-3); tm_q / tm_k 4D maps as in assign
+cudaError_t launch_attention_density(const CUtensorMap* tm_q, const CUtensorMap* tm_k, int B, int H, int N, int d,
+                                     float scale, double tau, int passes, float* row_m, float* row_z, float* row_lo,
+                                     float* row_hi, int32_t* counts, double* density, cudaStream_t st);
+
 }  // namespace cs

@@ -130,7 +130,10 @@ def run_layers(a):
     dev = torch.device("cuda", 0)
     c = CONFIGS[a.config]
     nl = a.layers
-    prof = synthetic_profile(nl, c["H"], seed=a.seed)  # [L, H]; layer 0 dense
+    if a.schedule:  # d_hat from the offline profiler (scripts/profile_schedule.py, NEXT-3)
+        prof = torch.tensor(json.load(open(a.schedule))["d_hat"], dtype=torch.float32)[:nl]
+    else:
+        prof = synthetic_profile(nl, c["H"], seed=a.seed)  # [L, H]; layer 0 dense
     sust, _ = peaks()
     ws = pb.Workspace()
     rows = []
@@ -160,6 +163,7 @@ def run_layers(a):
     ms = np.array([r["ms_layer"] for r in rows])
     fr = np.array([r["roofline_frac_sustained"] for r in rows])
     summ = {"config": a.config, "rule": "density", "tau": a.tau, "theta": a.theta, "sel_flags": a.sel_flags,
+            "budgets": a.schedule or "synthetic_profile",
             "layers": nl,
             "ms_layer_mean": float(ms.mean()), "ms_layer_min": float(ms.min()), "ms_layer_max": float(ms.max()),
             "ms_layer_mean_excl_dense_layer0": float(ms[1:].mean()) if nl > 1 else None,
@@ -183,6 +187,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--sel-flags", type=int, default=0, help="NEXT-4 selection variants (layers mode)")
+    ap.add_argument("--schedule", default=None, help="layers mode: budgets = d_hat of a profiler schedule JSON")
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
     t0 = time.time()
