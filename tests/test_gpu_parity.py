@@ -531,3 +531,23 @@ def test_kmeans_assign_chain_teacher_forced_and_layer(pb):
         for j in np.unique(Lh):
             m = X[Lh == j].mean(0)
             assert np.allclose(Ch[j], m, rtol=1e-5, atol=1e-5), side
+
+
+def test_streamed_layer_matches_direct_calls(pb):
+    """runtime.StreamedLayer (upload / layer / download on three streams, two buffer sets) returns
+    exactly the outputs of direct calls, for more calls than buffer sets."""
+    from paper_2603_18636_b200.runtime import StreamedLayer
+    budget = torch.tensor([0.3, 0.5], dtype=torch.float32).cuda()
+    ins = [video_qkv(4, 16, 16, 2, 128, seed=40 + i) for i in range(5)]
+    ref = [pb.coclust_sparse_attention(w.q.cuda(), w.k.cuda(), w.v.cuda(), 12, 40, 2, budget).cpu() for w in ins]
+    pinned = [tuple(t.pin_memory() for t in (w.q, w.k, w.v)) for w in ins]
+    outs = [torch.empty_like(ins[0].q).pin_memory() for _ in ins]
+    ws = pb.Workspace()
+    sl = StreamedLayer(lambda dq, dk, dv, do: pb.coclust_sparse_attention(dq, dk, dv, 12, 40, 2, budget, out=do,
+                                                                         ws=ws),
+                       ins[0].q.shape, "cuda", depth=2)
+    for i, (hq, hk, hv) in enumerate(pinned):
+        sl.submit(i, hq, hk, hv, outs[i])
+    torch.cuda.synchronize()
+    for o, r in zip(outs, ref):
+        assert torch.equal(o, r)
