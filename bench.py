@@ -53,6 +53,9 @@ def parse():
                          "256 = independent k-means partitioning (w/o On baseline, NEXT-2)")
     ap.add_argument("--parallel", choices=["head", "ulysses"], default=None,
                     help="multi-GPU split (default: ulysses for hunyuan_720p, head-parallel otherwise)")
+    ap.add_argument("--ulysses-return", choices=["fused", "nccl"], default="fused",
+                    help="Ulysses output path: attention epilogue stores into the owners' token blocks "
+                         "(fused, CUDA IPC / NVLink) or NCCL all_to_all + unpack")
     ap.add_argument("--cpu-sample-rows", type=int, default=1500,
                     help="query rows of the oracle attention sample")
     return ap.parse_args()
@@ -215,10 +218,18 @@ def run_ours(args):
         q, k, v = tok(full.q), tok(full.k), tok(full.v)          # [1, N/P, H, d] token blocks
         q_h, k_h = full.q[:, h0:h1].contiguous(), full.k[:, h0:h1].contiguous()  # for F_kept only
         kw = dict(seed=args.seed, tau=args.tau, theta=args.theta, rule=rule, ws=ws)
+        if args.ulysses_return == "fused":
+            from paper_2603_18636_b200.dist import PeerOutput, ulysses_layer_fused
+            peer = PeerOutput(Nl, H_total, d, dev)
 
-        def step(evs=None, qq=None, kk_=None, vv=None):
-            return ulysses_layer(q if qq is None else qq, k if kk_ is None else kk_, v if vv is None else vv,
-                                 args.kq, args.kk, args.iters, budget_all, stage_events=evs, **kw)
+            def step(evs=None, qq=None, kk_=None, vv=None):
+                return ulysses_layer_fused(q if qq is None else qq, k if kk_ is None else kk_,
+                                           v if vv is None else vv, args.kq, args.kk, args.iters, budget_all, peer,
+                                           stage_events=evs, **kw)
+        else:
+            def step(evs=None, qq=None, kk_=None, vv=None):
+                return ulysses_layer(q if qq is None else qq, k if kk_ is None else kk_, v if vv is None else vv,
+                                     args.kq, args.kk, args.iters, budget_all, stage_events=evs, **kw)
     else:
         h0, h1 = head_range(H_total, world, rank)
         q, k, v = (t[:, h0:h1].contiguous() for t in (full.q, full.k, full.v))
@@ -400,7 +411,8 @@ def run_ours(args):
         "config": {"workload": CONFIG_NAMES[args.config], "B": B, "H": H_total, "N": N, "d": d,
                    "kq": args.kq, "kk": args.kk, "iters": args.iters, "budget": args.budget,
                    "rule": args.rule, "tau": args.tau, "theta": args.theta, "sel_flags": args.sel_flags,
-                   "parallelism": (f"ulysses-a2a x{world}" if mode == "ulysses" else f"head-parallel x{world}"),
+                   "parallelism": (f"ulysses-a2a x{world} (return: {args.ulysses_return})" if mode == "ulysses"
+                                   else f"head-parallel x{world}"),
                    "l2": "inputs larger than L2 (%.0f MB/tensor/rank)" % (q.numel() * 2 / 1e6)},
         "kept_tflop_per_layer": f_kept_total / 1e12,
         "kept_frac": f_kept_total / dense_flops,

@@ -251,6 +251,44 @@ cs_status attention_density(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in
                             float scale, int passes, int32_t* counts, double* density, void* ws,
                             size_t ws_bytes, void* stream);
 
+/* ---- Fused Ulysses return path: the attention epilogue stores each output row
+ * straight into the token block of the rank that owns the token (NVLink P2P / CUDA IPC mapped
+ * pointers), fusing the inverse permutation AND the return all-to-all into the attention kernel.
+ * Rank p's output block is [N/P, H_total, d] bf16 with element strides s_tok (token) and s_head
+ * (head), d contiguous; token n of this call goes to rank n / n_per_rank, row n % n_per_rank,
+ * head head_base + h. */
+typedef struct {
+  const void* ptrs;    /* DEVICE array of P uint64 device pointers (peer blocks mapped here) */
+  int P;               /* ranks; P * n_per_rank == N */
+  int n_per_rank;
+  int head_base;       /* global head index of this call's head 0 */
+  int64_t s_tok, s_head;
+} cs_peer_out;
+
+/* coclust_sparse_attention (B = 1) with its output scattered to the peers' token blocks.  The
+ * caller orders the consumers after all ranks' calls, e.g. with cs_peer_barrier on the stream. */
+cs_status coclust_sparse_attention_peer(int H, int N, int d, cs_bf16_in q, cs_bf16_in k,
+                                        cs_bf16_in v, int kq, int kk, int iters, uint64_t seed,
+                                        int head_offset, int heads_total, const float* budget,
+                                        double tau, double theta, int rule, int flags, float scale,
+                                        const cs_peer_out* o, void* ws, size_t ws_bytes,
+                                        void* stream, void* const* stage_events);
+
+/* Device-side barrier over P ranks: peer_flags = DEVICE array of P uint64 pointers to every
+ * rank's int32 flag array [P] (zero-initialised, mapped here); rank `rank` writes `epoch` into
+ * flags_p[rank] of every rank p (system-scope release) after all earlier work on `stream`, then
+ * waits until its own flags[p] >= epoch for all p (acquire).  epoch >= 1, increasing per use.
+ * A peer that never arrives makes the kernel trap after ~2^32 cycles (launch error, no hang). */
+cs_status cs_peer_barrier(int P, int rank, const void* peer_flags, int epoch, void* stream);
+
+/* CUDA IPC export / import of caller-owned device memory: handle_out receives the 64-byte
+ * cudaIpcMemHandle of the allocation containing dev_ptr and offset_out dev_ptr's offset in it;
+ * cs_ipc_open maps a peer's handle (lazy peer access) and returns the peer pointer (base +
+ * offset); cs_ipc_close unmaps it. */
+cs_status cs_ipc_handle(const void* dev_ptr, void* handle_out, size_t* offset_out);
+cs_status cs_ipc_open(const void* handle, size_t offset, void** dev_ptr_out);
+cs_status cs_ipc_close(void* dev_ptr, size_t offset);
+
 /* Ulysses resharding helper (BASELINE configs[3]): dst[b][a] = src[a][b] for an
  * [A, B] grid of rows of row_bytes bytes (row_bytes a multiple of 16, pointers 16-byte aligned).
  * Packs a [N/P, H, d] token block into [P, N/P, H/P, d] per-destination chunks before the

@@ -73,6 +73,13 @@ _SIG = {
                                          _I, ctypes.c_float, _BF16Out, _P, ctypes.c_size_t, _P, _P]),
     "cs_block_transpose": (_I, [_I, _I, ctypes.c_size_t, _P, _P, _P]),
     "cs_density_workspace_bytes": (ctypes.c_size_t, [_I, _I, _I]),
+    "coclust_sparse_attention_peer": (_I, [_I, _I, _I, _BF16In, _BF16In, _BF16In, _I, _I, _I, ctypes.c_uint64, _I,
+                                           _I, _P, ctypes.c_double, ctypes.c_double, _I, _I, ctypes.c_float, _P, _P,
+                                           ctypes.c_size_t, _P, _P]),
+    "cs_peer_barrier": (_I, [_I, _I, _P, _I, _P]),
+    "cs_ipc_handle": (_I, [_P, _P, ctypes.POINTER(ctypes.c_size_t)]),
+    "cs_ipc_open": (_I, [_P, ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)]),
+    "cs_ipc_close": (_I, [_P, ctypes.c_size_t]),
     "attention_density": (_I, [_I, _I, _I, _I, _BF16In, _BF16In, ctypes.c_double, ctypes.c_float, _I, _P, _P, _P,
                                ctypes.c_size_t, _P]),
     "coclust_sparse_attention_cached": (_I, [_I, _I, _I, _I, _BF16In, _BF16In, _BF16In, _I, _I, _I,
@@ -309,6 +316,55 @@ def attention_density(q, k, tau=0.95, scale=None, passes=0, counts=False, ws=Non
     _check(lib().attention_density(B, H, N, d, _bf16(q), _bf16(k), float(tau), float(scale), int(passes),
                                    _ptr(cnt), _ptr(dens), w, wn, _stream(q)))
     return (dens, cnt) if counts else dens
+
+
+class _PeerOut(ctypes.Structure):
+    _fields_ = [("ptrs", ctypes.c_void_p), ("P", ctypes.c_int), ("n_per_rank", ctypes.c_int),
+                ("head_base", ctypes.c_int), ("s_tok", ctypes.c_int64), ("s_head", ctypes.c_int64)]
+
+
+def coclust_sparse_attention_peer(q, k, v, kq, kk, iters, budget, *, peer_ptrs, P, n_per_rank, head_base,
+                                  s_tok, s_head, seed=0, tau=0.95, theta=0.1, rule=RULE_DENSITY, flags=0,
+                                  scale=None, ws=None, head_offset=0, heads_total=0, stage_events=None):
+    """The layer (B = 1) with every output row stored straight into the token block of the rank
+    that owns the token (fused Ulysses return all-to-all).  peer_ptrs: int64 device tensor [P]."""
+    _cuda(q, "q")
+    B, H, N, d = q.shape
+    if B != 1:
+        raise ValueError("peer-output layer needs B == 1")
+    scale = d ** -0.5 if scale is None else scale
+    w, wn = _ws(ws, workspace_bytes(B, H, N, d, kq, kk), q.device)
+    po = _PeerOut(peer_ptrs.data_ptr(), P, n_per_rank, head_base, s_tok, s_head)
+    evs = None
+    if stage_events is not None:
+        evs = (ctypes.c_void_p * 4)(*[ctypes.c_void_p(e.cuda_event) for e in stage_events])
+    _check(lib().coclust_sparse_attention_peer(H, N, d, _bf16(q), _bf16(k), _bf16(v), kq, kk, iters, seed,
+                                               head_offset, heads_total, _ptr(budget), float(tau), float(theta),
+                                               int(rule), int(flags), float(scale), ctypes.byref(po), w, wn,
+                                               _stream(q), evs))
+
+
+def peer_barrier(P, rank, flag_ptrs, epoch, stream_of):
+    """Device-side barrier over the peers' flag arrays (flag_ptrs: int64 device tensor [P])."""
+    _check(lib().cs_peer_barrier(P, rank, _ptr(flag_ptrs), int(epoch), _stream(stream_of)))
+
+
+def ipc_handle(t):
+    """-> (64-byte cudaIpcMemHandle of t's allocation, byte offset of t in it)."""
+    h = ctypes.create_string_buffer(64)
+    off = ctypes.c_size_t(0)
+    _check(lib().cs_ipc_handle(_ptr(t), h, ctypes.byref(off)))
+    return h.raw, int(off.value)
+
+
+def ipc_open(handle: bytes, offset: int) -> int:
+    p = ctypes.c_void_p(0)
+    _check(lib().cs_ipc_open(ctypes.create_string_buffer(handle, 64), offset, ctypes.byref(p)))
+    return int(p.value)
+
+
+def ipc_close(ptr: int, offset: int):
+    _check(lib().cs_ipc_close(ctypes.c_void_p(ptr), offset))
 
 
 def block_transpose(src, A, B, out=None):

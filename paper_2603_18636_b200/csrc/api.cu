@@ -273,7 +273,8 @@ cs_status run_assign(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in k, int
 
 cs_status run_attn(int B, int H, int N, int d, int kq, int kk, const int32_t* perm_q, const int32_t* offs_q,
                    const int32_t* offs_k, const int32_t* n_keep, const int32_t* n_rows, const int32_t* kept, float scale,
-                   cs_bf16_out o, const AttnScratch& sc, cudaStream_t st, void* const* ev = nullptr) {
+                   cs_bf16_out o, const AttnScratch& sc, cudaStream_t st, void* const* ev = nullptr,
+                   const cs_peer_out* po = nullptr) {
   const int BH = B * H;
   CS_CUDA(launch_worklist(BH, kq, offs_q, sc.item_start, st), "worklist");
   CUtensorMap tq;
@@ -286,7 +287,9 @@ cs_status run_attn(int B, int H, int N, int d, int kq, int kk, const int32_t* pe
   if (ev) CS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(ev[2]), st), "event");
   CS_CUDA(launch_bsa_fwd(&tq, &kv, BH, H, N, d, kq, kk, perm_q, offs_q, offs_k, n_keep, n_rows, kept,
                          sc.item_start, worklist_upper_bound(N, kq), scale,
-                         static_cast<__nv_bfloat16*>(o.ptr), o.sb, o.sh, o.sn, st),
+                         static_cast<__nv_bfloat16*>(o.ptr), o.sb, po ? po->s_head : o.sh,
+                         po ? po->s_tok : o.sn, po ? static_cast<const uint64_t*>(po->ptrs) : nullptr,
+                         po ? po->n_per_rank : 0, po ? po->head_base : 0, st),
           "bsa_fwd");
   if (ev) CS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(ev[3]), st), "event");
   return CS_OK;
@@ -524,7 +527,7 @@ cs_status check_layer_args(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in 
 cs_status run_layer(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in k, cs_bf16_in v, int kq, int kk,
                     int iters, uint64_t seed, int head_offset, int heads_total, const float* budget, double tau,
                     double theta, int rule, int sel_flags, float scale, cs_bf16_out o, const LayerState& s, bool recompute,
-                    Carve& c, cudaStream_t st, void* const* ev) {
+                    Carve& c, cudaStream_t st, void* const* ev, const cs_peer_out* po = nullptr) {
   const int BH = B * H;
   AttnScratch at = carve_attn(c, BH, N, d, kq);
   AssignScratch as = carve_assign(c, BH, N, d, kq, kk);
@@ -548,7 +551,7 @@ cs_status run_layer(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in k, cs_b
   }
   CS_CUDA(launch_permute_rows(view(v, H), BH, N, d, s.perm_k, at.vp, st), "permute_v");
   return run_attn(B, H, N, d, kq, kk, s.perm_q, s.offs_q, s.offs_k, s.n_keep, s.n_rows, s.kept, scale, o, at, st,
-                  ev);
+                  ev, po);
 }
 }  // namespace
 
@@ -639,6 +642,81 @@ cs_status attention_density(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in
   CS_CUDA(launch_attention_density(&tq, &tk, B, H, N, d, scale, tau, passes, st4, st4 + rows, st4 + 2 * rows,
                                    st4 + 3 * rows, counts ? counts : cnt, density, static_cast<cudaStream_t>(stream)),
           "attention_density");
+  return CS_OK;
+}
+
+cs_status coclust_sparse_attention_peer(int H, int N, int d, cs_bf16_in q, cs_bf16_in k, cs_bf16_in v, int kq,
+                                        int kk, int iters, uint64_t seed, int head_offset, int heads_total,
+                                        const float* budget, double tau, double theta, int rule, int flags,
+                                        float scale, const cs_peer_out* o, void* ws, size_t ws_bytes, void* stream,
+                                        void* const* stage_events) {
+  g_err[0] = 0;
+  NEED(o, "o");
+  NEED(o->ptrs, "o->ptrs");
+  if (o->P < 1 || o->n_per_rank < 1 || (long long)o->P * o->n_per_rank != N)
+    return fail(CS_ERR_SHAPE, "peer output: P * n_per_rank must equal N (%d * %d vs %d)", o->P, o->n_per_rank, N);
+  if (o->head_base < 0 || o->s_tok <= 0 || o->s_head <= 0 || o->s_tok % 8 || o->s_head % 8)
+    return fail(CS_ERR_ALIGN, "peer output: strides must be positive multiples of 8 elements");
+  cs_bf16_out dummy{const_cast<void*>(o->ptrs), 0, o->s_head, o->s_tok};  // validated like an output, never stored to
+  CS_CHECK(check_layer_args(1, H, N, d, q, k, v, kq, kk, iters, head_offset, heads_total, budget, tau, theta,
+                            rule, flags, scale, dummy));
+  CS_CHECK(check_ws(ws, ws_bytes, need_layer(H, N, d, kq, kk)));
+  Carve c(ws);
+  LayerState s = carve_state(c, H, N, d, kq, kk);
+  return run_layer(1, H, N, d, q, k, v, kq, kk, iters, seed, head_offset, heads_total, budget, tau, theta, rule,
+                   flags, scale, dummy, s, true, c, static_cast<cudaStream_t>(stream), stage_events, o);
+}
+
+cs_status cs_peer_barrier(int P, int rank, const void* peer_flags, int epoch, void* stream) {
+  g_err[0] = 0;
+  if (P < 1 || P > 32 || rank < 0 || rank >= P) return fail(CS_ERR_ARG, "need 1 <= P <= 32, 0 <= rank < P");
+  if (epoch < 1) return fail(CS_ERR_ARG, "epoch must be >= 1 (flags start at 0)");
+  NEED(peer_flags, "peer_flags");
+  CS_CUDA(launch_peer_barrier(P, rank, static_cast<const uint64_t*>(peer_flags), epoch,
+                              static_cast<cudaStream_t>(stream)),
+          "peer_barrier");
+  return CS_OK;
+}
+
+typedef CUresult (*PtrAttrFn)(void*, CUpointer_attribute, CUdeviceptr);
+
+cs_status cs_ipc_handle(const void* dev_ptr, void* handle_out, size_t* offset_out) {
+  g_err[0] = 0;
+  NEED(dev_ptr, "dev_ptr"); NEED(handle_out, "handle_out"); NEED(offset_out, "offset_out");
+  static PtrAttrFn attr = nullptr;
+  if (!attr) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuPointerGetAttribute", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      attr = reinterpret_cast<PtrAttrFn>(p);
+  }
+  if (!attr) return fail(CS_ERR_CUDA, "cuPointerGetAttribute unavailable");
+  CUdeviceptr base = 0;
+  if (attr(&base, CU_POINTER_ATTRIBUTE_RANGE_START_ADDR, reinterpret_cast<CUdeviceptr>(dev_ptr)) != CUDA_SUCCESS)
+    return fail(CS_ERR_CUDA, "cuPointerGetAttribute(RANGE_START_ADDR) failed");
+  cudaIpcMemHandle_t h;
+  CS_CUDA(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)), "cudaIpcGetMemHandle");
+  memcpy(handle_out, &h, sizeof(h));
+  *offset_out = reinterpret_cast<uintptr_t>(dev_ptr) - static_cast<uintptr_t>(base);
+  return CS_OK;
+}
+
+cs_status cs_ipc_open(const void* handle, size_t offset, void** dev_ptr_out) {
+  g_err[0] = 0;
+  NEED(handle, "handle"); NEED(dev_ptr_out, "dev_ptr_out");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  void* base = nullptr;
+  CS_CUDA(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+  *dev_ptr_out = static_cast<uint8_t*>(base) + offset;
+  return CS_OK;
+}
+
+cs_status cs_ipc_close(void* dev_ptr, size_t offset) {
+  g_err[0] = 0;
+  NEED(dev_ptr, "dev_ptr");
+  CS_CUDA(cudaIpcCloseMemHandle(static_cast<uint8_t*>(dev_ptr) - offset), "cudaIpcCloseMemHandle");
   return CS_OK;
 }
 

@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               const int32_t* __restrict__ n_rows, const int32_t* __restrict__ kept,
               const int32_t* __restrict__ item_start,
               float scale_log2, __nv_bfloat16* __restrict__ out, long long osb, long long osh,
-              long long osn) {
+              long long osn, const uint64_t* __restrict__ peer_ptrs, int peer_npr, int peer_head_base) {
   using L = Smem<D>;
   extern __shared__ uint8_t smem_raw[];
   // align to 1024 B while keeping the pointer in the shared window (LDS/STS, not generic LD/ST)
@@ -483,7 +483,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const bool row_ok = prow < qlen;
       const int tok = row_ok ? perm_q[(size_t)bh * N + qbeg + prow] : 0;
       const int b = bh / H, h = bh % H;
-      __nv_bfloat16* dst = out + (long long)b * osb + (long long)h * osh + (long long)tok * osn;
+      __nv_bfloat16* dst;
+      if (peer_ptrs) {
+        // fused Ulysses return all-to-all: token tok lives on rank tok / npr, whose [N/P, H_total,
+        // d] token block is mapped into this process (NVLink P2P / CUDA IPC); head h of this call
+        // is global head peer_head_base + h.  The 16-byte row stores go straight to the peer.
+        const int pr = tok / peer_npr;
+        dst = reinterpret_cast<__nv_bfloat16*>(peer_ptrs[pr]) + (long long)(tok - pr * peer_npr) * osn +
+              (long long)(peer_head_base + h) * osh;
+      } else {
+        dst = out + (long long)b * osb + (long long)h * osh + (long long)tok * osn;
+      }
       if (split && nt > 1) {
         // merge the two partial states of the row (each relative to its own running max):
         // O = (O0 2^(m0-M) + O1 2^(m1-M)) / (l0 2^(m0-M) + l1 2^(m1-M)); set tq writes the
@@ -556,7 +566,8 @@ cudaError_t launch_bsa_fwd(const CUtensorMap* tm_q, const KVMaps* kv,
                            const int32_t* offs_q, const int32_t* offs_k, const int32_t* n_keep,
                            const int32_t* n_rows, const int32_t* kept, const int32_t* item_start, int items_ub,
                            float scale, __nv_bfloat16* o, long long osb, long long osh,
-                           long long osn, cudaStream_t st) {
+                           long long osn, const uint64_t* peer_ptrs, int peer_npr, int peer_head_base,
+                           cudaStream_t st) {
   const float scale_log2 = scale * 1.4426950408889634f;
   dim3 grid(items_ub, BH);
   if (d == 128) {
@@ -565,14 +576,16 @@ cudaError_t launch_bsa_fwd(const CUtensorMap* tm_q, const KVMaps* kv,
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     kfn<<<grid, attn::NTHREADS, smem, st>>>(*tm_q, *kv, H, N, kq, kk, perm_q, offs_q, offs_k,
-                                           n_keep, n_rows, kept, item_start, scale_log2, o, osb, osh, osn);
+                                           n_keep, n_rows, kept, item_start, scale_log2, o, osb, osh, osn,
+                                           peer_ptrs, peer_npr, peer_head_base);
   } else {
     auto kfn = attn::k_bsa_fwd<64>;
     const int smem = attn::Smem<64>::ALLOC;
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     kfn<<<grid, attn::NTHREADS, smem, st>>>(*tm_q, *kv, H, N, kq, kk, perm_q, offs_q, offs_k,
-                                           n_keep, n_rows, kept, item_start, scale_log2, o, osb, osh, osn);
+                                           n_keep, n_rows, kept, item_start, scale_log2, o, osb, osh, osn,
+                                           peer_ptrs, peer_npr, peer_head_base);
   }
   return cudaGetLastError();
 }

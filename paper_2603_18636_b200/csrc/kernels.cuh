@@ -70,7 +70,11 @@ cudaError_t launch_bsa_fwd(const CUtensorMap* tm_q, const KVMaps* kv,
                            const int32_t* offs_q, const int32_t* offs_k, const int32_t* n_keep,
                            const int32_t* n_rows, const int32_t* kept, const int32_t* item_start, int items_ub,
                            float scale, __nv_bfloat16* o, long long osb, long long osh,
-                           long long osn, cudaStream_t st);
+                           long long osn, const uint64_t* peer_ptrs, int peer_npr,
+                           int peer_head_base, cudaStream_t st);
+
+// ---- peer.cu : cross-process peer memory (CUDA IPC) and a device-side barrier over peer flags
+cudaError_t launch_peer_barrier(int P, int rank, const uint64_t* peer_flags, int epoch, cudaStream_t st);
 
 // ---- profile.cu : offline attention density (NEXT-3); tm_q / tm_k 4D maps as in assign
 cudaError_t launch_attention_density(const CUtensorMap* tm_q, const CUtensorMap* tm_k, int B, int H, int N, int d,

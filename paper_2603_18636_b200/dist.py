@@ -10,6 +10,12 @@ V.  One all_to_all_single per tensor (NCCL over NVLink) turns it into all N toke
 the layer runs on those heads (the ABI takes the [N, H/P, d] buffer through strides, no copy);
 one all_to_all_single brings O back to the token block.  The only data movement besides the
 collectives is the pack / unpack block transpose (cs_block_transpose, our kernel).
+
+Fused return path (`ulysses_layer_fused`): the output token blocks of all ranks are mapped into
+every process (CUDA IPC; over NVLink on a multi-GPU box) and the attention epilogue stores each
+output row straight into the block of the rank that owns its token — the inverse permutation,
+the return all-to-all and the unpack become the attention kernel's own stores.  A device-side
+barrier over peer flags (cs_peer_barrier) orders the consumer after every rank's epilogue.
 """
 from __future__ import annotations
 
@@ -85,3 +91,76 @@ def ulysses_layer(q_loc, k_loc, v_loc, kq, kk, iters, budget, *, group=None, tra
     # unpack: [P, Nl, Hl, d] -> [Nl, P, Hl, d] = [Nl, H, d]
     o_loc = transpose(back.view(P, Nl * Hl * d), P, Nl)
     return o_loc.view(1, Nl, H, d)
+
+
+class PeerOutput:
+    """This rank's output token block [1, N/P, H, d] (bf16) and flag array, mapped into every rank
+    of `group` by CUDA IPC; `ptrs` / `flag_ptrs` are int64 device tensors [P] of the mapped
+    addresses (this rank's own entry is its local pointer)."""
+
+    def __init__(self, Nl, H, d, device, group=None):
+        import torch
+        import torch.distributed as dist
+        import paper_2603_18636_b200 as pb
+        self.P = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.out = torch.zeros(1, Nl, H, d, dtype=torch.bfloat16, device=device)
+        self.flags = torch.zeros(self.P, dtype=torch.int32, device=device)
+        torch.cuda.synchronize(device)
+        mine = (pb.ipc_handle(self.out), pb.ipc_handle(self.flags)) if self.P > 1 else None
+        allh = [None] * self.P
+        dist.all_gather_object(allh, mine, group=group)
+        self._opened = []
+        optrs, fptrs = [], []
+        for p in range(self.P):
+            if p == self.rank:
+                optrs.append(self.out.data_ptr())
+                fptrs.append(self.flags.data_ptr())
+                continue
+            (ho, oo), (hf, of) = allh[p]
+            po, pf = pb.ipc_open(ho, oo), pb.ipc_open(hf, of)
+            self._opened += [(po, oo), (pf, of)]
+            optrs.append(po)
+            fptrs.append(pf)
+        as_i64 = lambda xs: torch.tensor([x if x < 2 ** 63 else x - 2 ** 64 for x in xs], dtype=torch.int64,
+                                         device=device)
+        self.ptrs, self.flag_ptrs = as_i64(optrs), as_i64(fptrs)
+        self.epoch = 0
+
+    def close(self):
+        import paper_2603_18636_b200 as pb
+        for p, off in self._opened:
+            pb.ipc_close(p, off)
+        self._opened = []
+
+
+def ulysses_layer_fused(q_loc, k_loc, v_loc, kq, kk, iters, budget, peer: "PeerOutput", *, group=None,
+                        a2a=None, **kw):
+    """ulysses_layer with the return all-to-all fused into the attention epilogue (see module doc).
+
+    Returns peer.out [1, N/P, H, d], complete once the calling stream passes the device barrier.
+    `a2a(recv, send)` overrides the input all_to_all_single (e.g. through host memory for a gloo
+    group in tests)."""
+    import torch
+    import torch.distributed as dist
+    import paper_2603_18636_b200 as pb
+    P = dist.get_world_size(group)
+    r = dist.get_rank(group)
+    B, Nl, H, d = q_loc.shape
+    if B != 1 or H % P:
+        raise ValueError("Ulysses path needs B == 1 and H divisible by the group size")
+    Hl = H // P
+    N = Nl * P
+    a2a = a2a or (lambda recv, send: dist.all_to_all_single(recv, send, group=group))
+    full = []
+    for x in (q_loc, k_loc, v_loc):
+        send = pb.block_transpose(x.contiguous().view(Nl, P * Hl * d), Nl, P)
+        recv = torch.empty_like(send)
+        a2a(recv, send)
+        full.append(recv.view(N, Hl, d).permute(1, 0, 2).unsqueeze(0))
+    pb.coclust_sparse_attention_peer(full[0], full[1], full[2], kq, kk, iters, budget[r * Hl:(r + 1) * Hl].contiguous(),
+                                     peer_ptrs=peer.ptrs, P=P, n_per_rank=Nl, head_base=r * Hl, s_tok=H * d,
+                                     s_head=d, head_offset=r * Hl, heads_total=H, **kw)
+    peer.epoch += 1
+    pb.peer_barrier(P, r, peer.flag_ptrs, peer.epoch, full[0])
+    return peer.out
