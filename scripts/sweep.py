@@ -175,6 +175,7 @@ def run_layers(a):
 
 
 def main():
+    from bench import ClockSampler
     ap = argparse.ArgumentParser()
     ap.add_argument("mode", choices=["cells", "layers"])
     ap.add_argument("--config", default="wan1.3b_480p")
@@ -191,7 +192,14 @@ def main():
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
     t0 = time.time()
+    clk = ClockSampler(0)
+    clk.start()
     (run_cells if a.mode == "cells" else run_layers)(a)
+    c = clk.stop()
+    print(json.dumps({"clocks": c}), flush=True)
+    if a.out:
+        with open(a.out, "a") as f:
+            f.write(json.dumps({"clocks": c}) + "\n")
     print(f"# wall {time.time() - t0:.1f} s", flush=True)
 
 
