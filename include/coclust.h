@@ -240,10 +240,11 @@ cs_status coclust_sparse_attention_cached(int B, int H, int N, int d, cs_bf16_in
  *   A = softmax(q k^T * scale) (rows), S(i) = the minimal descending prefix of row i whose mass
  *   reaches tau (R9b tolerance 1e-12), counts[b][h][i] = |S(i)| (nullable [B,H,N] int32 out),
  *   density[b][h] = (1/N) sum_i |S(i)| / N (double out [B,H]).
- * No sort: after a row max / row sum pass, `passes` binning passes (0 -> 4) narrow the crossing of
- * the descending cumulative mass to a log2-interval of width 65 / 32^passes; the count inside the
- * final interval is interpolated from its elements' mean mass (exact unless several elements
- * share that interval).  Each pass recomputes Q K^T on the tensor cores.  The Gaussian fit over
+ * No sort: after a row max / row sum pass, `passes` (0 -> 4, at most 5) radix passes over the float
+ * bits of p = 2^(logit - max) (exponent, then 5 mantissa bits per pass) locate the crossing of the
+ * descending cumulative mass to p-values sharing exponent and 5 (passes-1) mantissa bits; the
+ * count inside that final bin is interpolated from its elements' mean mass (exact unless several
+ * elements share the bin).  Each pass recomputes Q K^T on the tensor cores.  The Gaussian fit over
  * calibration inputs and the schedule s = 1 - d_hat are host-side
  * (paper_2603_18636_b200/profiler.py).  Workspace: cs_density_workspace_bytes(B, H, N). */
 size_t cs_density_workspace_bytes(int B, int H, int N);

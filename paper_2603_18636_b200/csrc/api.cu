@@ -615,7 +615,7 @@ size_t cs_density_workspace_bytes(int B, int H, int N) {
   if (B <= 0 || H <= 0 || N <= 0) return 0;
   Carve c(nullptr);
   const size_t rows = (size_t)B * H * N;
-  c.take<float>(4 * rows);
+  c.take<float>(6 * rows);
   c.take<int32_t>(rows);
   return c.off + 256;
 }
@@ -629,18 +629,18 @@ cs_status attention_density(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in
   if (!(tau > 0.0 && tau <= 1.0)) return fail(CS_ERR_ARG, "tau must be in (0, 1] (got %g)", tau);
   if (!(scale > 0.f)) return fail(CS_ERR_ARG, "scale must be > 0 (got %g)", (double)scale);
   if (passes == 0) passes = 4;
-  if (passes < 1 || passes > 8) return fail(CS_ERR_ARG, "passes must be in [1, 8] (got %d)", passes);
+  if (passes < 1 || passes > 5) return fail(CS_ERR_ARG, "passes must be in [1, 5] (got %d)", passes);
   NEED(density, "density");
   CS_CHECK(check_ws(ws, ws_bytes, cs_density_workspace_bytes(B, H, N)));
   Carve c(ws);
   const size_t rows = (size_t)B * H * N;
-  float* st4 = c.take<float>(4 * rows);
+  float* st6 = c.take<float>(6 * rows);
   int32_t* cnt = c.take<int32_t>(rows);
   CUtensorMap tq, tk;
   CS_CHECK(make_map_x(&tq, q, B, H, N, d));
   CS_CHECK(make_map_x(&tk, k, B, H, N, d));
-  CS_CUDA(launch_attention_density(&tq, &tk, B, H, N, d, scale, tau, passes, st4, st4 + rows, st4 + 2 * rows,
-                                   st4 + 3 * rows, counts ? counts : cnt, density, static_cast<cudaStream_t>(stream)),
+  CS_CUDA(launch_attention_density(&tq, &tk, B, H, N, d, scale, tau, passes, st6, rows, counts ? counts : cnt,
+                                   density, static_cast<cudaStream_t>(stream)),
           "attention_density");
   return CS_OK;
 }

@@ -78,7 +78,7 @@ cudaError_t launch_peer_barrier(int P, int rank, const uint64_t* peer_flags, int
 
 // ---- profile.cu : offline attention density (NEXT-3); tm_q / tm_k 4D maps as in assign
 cudaError_t launch_attention_density(const CUtensorMap* tm_q, const CUtensorMap* tm_k, int B, int H, int N, int d,
-                                     float scale, double tau, int passes, float* row_m, float* row_z, float* row_lo,
-                                     float* row_hi, int32_t* counts, double* density, cudaStream_t st);
+                                     float scale, double tau, int passes, float* rs, size_t rows, int32_t* counts,
+                                     double* density, cudaStream_t st);
 
 }  // namespace cs

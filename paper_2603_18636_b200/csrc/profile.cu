@@ -2,14 +2,19 @@
 //
 // Attention density of one head: d = (1/N) sum_i |S(i)| / N, where S(i) is the minimal descending
 // prefix of row i of A = softmax(q k^T * scale) whose mass reaches tau (R9b tolerance 1e-12).
-// A full per-row sort over N = 75,600 columns is replaced by a threshold search in the exp2
-// domain (x_ij = s_ij * scale * log2(e) - m_i, p_ij = 2^x_ij / Z_i):
-//   pass 0      : row max m_i and Z_i = sum_j 2^x_ij                      (online, like flash)
-//   passes 1..P : the search interval [lo_i, hi_i) (initially [-64, 1)) is cut into 32 bins;
-//                 every element adds 2^x to "above" (x >= hi) or to its bin (count + mass), and
-//                 the bin where the descending cumulative mass crosses tau Z_i becomes the next
-//                 interval (width 65 / 32^p).  The last pass converts the crossing bin into a
-//                 count: elements above + ceil(residual mass / mean mass of the bin's elements).
+// A full per-row sort over N = 75,600 columns is replaced by a radix select on the float bits of
+// the unnormalised probabilities p_ij = 2^(s_ij * scale * log2(e) - m_i) in (0, 1] (positive
+// floats order like their bit patterns):
+//   pass 0      : row max m_i and Z_i = sum_j p_ij                          (online, like flash)
+//   pass 1      : 32 bins by the exponent of p (2^-32 < p <= 1; smaller p carry < 1e-4 of the mass
+//                 at N <= 2^17, so the tau crossing is never below them); every element adds p and
+//                 1 to its bin, the bin where the descending cumulative mass crosses tau Z_i
+//                 becomes the prefix of the next pass, the bins above it are carried (mass, count)
+//   pass k >= 2 : 32 bins by the next 5 mantissa bits among the elements matching the prefix
+//                 (one AND/XOR and a min per element; a 32-column chunk of a thread without a
+//                 match skips the binning)
+//   the last pass converts the crossing bin (p known to 5 (P-1) mantissa bits) into a count:
+//   elements above + ceil(residual mass / mean mass of the bin's elements).
 // Each pass recomputes S = Q K^T with tcgen05 (QK only: no PV, no P): one CTA = two 128-row Q
 // tiles of one head against every 128-key tile (2-slot TMA ring, TMEM double-buffered S for both
 // tiles), 8 row-worker warps (thread = query row = TMEM lane) + 1 TMA producer + 1 MMA warp.
@@ -21,7 +26,6 @@ namespace dens {
 
 constexpr int BM = 128, BN = 128, NST = 2, NBIN = 32, NTHREADS = 320;
 constexpr int WARP_PRODUCER = 8, WARP_MMA = 9;
-constexpr float kLo0 = -64.f, kHi0 = 1.f;  // initial search interval (log2 units below the row max)
 
 template <int D>
 struct Smem {
@@ -30,9 +34,8 @@ struct Smem {
   static constexpr int HALF_Q = BM * 128, HALF_K = BN * 128;
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_K = OFF_Q + 2 * QT;
-  static constexpr int OFF_MASS = OFF_K + NST * KT;              // float [NBIN][2 BM]
-  static constexpr int OFF_CNT = OFF_MASS + NBIN * 2 * BM * 4;   // int   [NBIN][2 BM]
-  static constexpr int OFF_BAR = OFF_CNT + NBIN * 2 * BM * 4;    // q_full, k_full[2], k_empty[2], s_full[2], s_empty[2]
+  static constexpr int OFF_BINS = OFF_K + NST * KT;              // float2 {mass, count bits} [NBIN][2 BM]
+  static constexpr int OFF_BAR = OFF_BINS + NBIN * 2 * BM * 8;   // q_full, k_full[2], k_empty[2], s_full[2], s_empty[2]
   static constexpr int OFF_MISC = OFF_BAR + 16 * 8;
   static constexpr int BYTES = OFF_MISC + 16;
   static constexpr int ALLOC = BYTES + 1024;
@@ -43,8 +46,15 @@ struct Smem {
 template <int D>
 __global__ void __launch_bounds__(NTHREADS, 1)
     k_density(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k, int H, int N,
-              float c, int pass, int last, double tau, float* __restrict__ row_m, float* __restrict__ row_z,
-              float* __restrict__ row_lo, float* __restrict__ row_hi, int32_t* __restrict__ counts) {
+              float c, int pass, int last, double tau, float* __restrict__ rs, size_t rows,
+              int32_t* __restrict__ counts) {
+  // per-row state [6][rows]: m, Z, lo, hi, mass above hi, count above hi (int bits)
+  float* row_m = rs;
+  float* row_z = rs + rows;
+  float* row_lo = rs + 2 * rows;
+  float* row_hi = rs + 3 * rows;
+  float* row_am = rs + 4 * rows;
+  int* row_an = reinterpret_cast<int*>(rs + 5 * rows);
   using L = Smem<D>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -54,8 +64,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint64_t* k_empty = bars + 3;
   uint64_t* s_full = bars + 5;
   uint64_t* s_empty = bars + 7;
-  float* bmass = reinterpret_cast<float*>(sm + L::OFF_MASS);
-  int* bcnt = reinterpret_cast<int*>(sm + L::OFF_CNT);
+  uint2* bins = reinterpret_cast<uint2*>(sm + L::OFF_BINS);  // .x = mass (fp32 bits), .y = count
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + L::OFF_MISC);
 
   const int bh = blockIdx.y, b = bh / H, h = bh % H;
@@ -128,52 +137,128 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const bool row_ok = n < N && (t == 0 || has1);
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
     const size_t ridx = (size_t)bh * N + (row_ok ? n : 0);
-    float m = -INFINITY, z = 0.f, lo = kLo0, hi = kHi0, inv_w = 0.f;
+    float m = -INFINITY, z = 0.f;
+    // radix state: elements with (bits(p) & pmask) == prefix are binned by (bits(p) >> sh) & 31
+    // (pass 1: the exponent, bins 0..31 = exponents 96..127)
+    uint32_t prefix = 0u, pmask = 0u;
+    const int sh = pass <= 1 ? 23 : 18 - 5 * (pass - 2);
     if (pass > 0) {
       m = row_ok ? row_m[ridx] : 0.f;
-      if (pass > 1 && row_ok) { lo = row_lo[ridx]; hi = row_hi[ridx]; }
-      inv_w = (float)NBIN / (hi - lo);
+      if (pass > 1) {
+        prefix = row_ok ? __float_as_uint(row_lo[ridx]) : 0xffffffffu;
+        pmask = 0xffffffffu << (sh + 5);
+      }
 #pragma unroll
-      for (int bi = 0; bi < NBIN; ++bi) { bmass[bi * 2 * BM + col] = 0.f; bcnt[bi * 2 * BM + col] = 0; }
+      for (int bi = 0; bi < NBIN; ++bi) bins[bi * 2 * BM + col] = make_uint2(0u, 0u);
     }
-    float above = 0.f;
+    float above = 0.f;  // mass / count of the elements above the current prefix (carried)
     int above_n = 0;
+    if (pass > 1 && row_ok) { above = row_am[ridx]; above_n = row_an[ridx]; }
+    auto bin_of = [&](uint32_t u) -> int {  // -1: not binned in this pass
+      if (pass == 1) {
+        const int e = (int)(u >> 23) - 96;
+        return e >= 0 ? min(e, NBIN - 1) : -1;
+      }
+      return (u & pmask) == prefix ? (int)((u >> sh) & 31u) : -1;
+    };
     for (int j = 0; j < nt; ++j) {
       const int buf = j & 1;
       mbar_wait(s_full + buf, (j >> 1) & 1);
       tc_fence_after();
-      uint32_t su[BN];
       const uint32_t s_tm = tmem + lane_off + (buf * 2 + t) * 128;
-#pragma unroll
-      for (int cc = 0; cc < BN / 32; ++cc) tmem_ld32(s_tm + cc * 32, su + cc * 32);
-      tmem_wait_ld();
-      tc_fence_before();
-      mbar_arrive(s_empty + buf);
       const int valid = min(BN, N - j * BN);  // columns past N (TMA zero fill) are ignored
-      if (pass == 0) {
-        float mx = -INFINITY;
+      float mx = -INFINITY;
+      if (pass == 0) {  // the row max of this tile first (a second TMEM read below)
+#pragma unroll 1
+        for (int cc = 0; cc < BN / 32; ++cc) {
+          uint32_t su[32];
+          tmem_ld32(s_tm + cc * 32, su);
+          tmem_wait_ld();
 #pragma unroll
-        for (int i = 0; i < BN; ++i) mx = fmaxf(mx, i < valid ? __uint_as_float(su[i]) : -INFINITY);
+          for (int i = 0; i < 32; ++i) mx = fmaxf(mx, cc * 32 + i < valid ? __uint_as_float(su[i]) : -INFINITY);
+        }
         const float mn = fmaxf(m, mx * c);
         z *= ex2(m - mn);  // m = -inf on the first tile: ex2(-inf) = 0
         m = mn;
-        float acc = 0.f;
+      }
+#pragma unroll 1
+      for (int cc = 0; cc < BN / 32; ++cc) {
+        uint32_t su[32];
+        tmem_ld32(s_tm + cc * 32, su);
+        tmem_wait_ld();
+        if (cc == BN / 32 - 1) {  // the S buffer is free for the MMA of tile j + 2
+          tc_fence_before();
+          mbar_arrive(s_empty + buf);
+        }
+        const bool tail = cc * 32 + 32 > valid;  // warp-uniform: only the last key tile has a tail
+        if (pass == 0) {
+          float acc = 0.f;
 #pragma unroll
-        for (int i = 0; i < BN; ++i)
-          acc += i < valid ? ex2(fmaf(__uint_as_float(su[i]), c, -m)) : 0.f;
-        z += acc;
-      } else {
-#pragma unroll
-        for (int i = 0; i < BN; ++i) {
-          const float x = i < valid ? fmaf(__uint_as_float(su[i]), c, -m) : -INFINITY;
-          if (x >= hi) {
-            above += ex2(x);
-            ++above_n;
-          } else if (x >= lo) {
-            const int bi = min(NBIN - 1, (int)((x - lo) * inv_w));
-            bmass[bi * 2 * BM + col] += ex2(x);
-            bcnt[bi * 2 * BM + col] += 1;
+          for (int i = 0; i < 32; ++i) {
+            const float e = ex2(fmaf(__uint_as_float(su[i]), c, -m));
+            acc += (!tail || cc * 32 + i < valid) ? e : 0.f;
           }
+          z += acc;
+          continue;
+        }
+        // p = 2^x as bits; columns past N -> 0 (never binned: exponent 0)
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const uint32_t u = __float_as_uint(ex2(fmaf(__uint_as_float(su[i]), c, -m)));
+          su[i] = (!tail || cc * 32 + i < valid) ? u : 0u;
+        }
+        if (pass > 1) {
+          // narrow prefix: few matches per row -> visit only those
+          uint32_t mn2 = 0xffffffffu;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) mn2 = min(mn2, (su[i] & pmask) ^ prefix);
+          if (mn2 != 0u) continue;  // no element of this thread's chunk matches
+          uint32_t inm = 0u;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) inm |= ((su[i] & pmask) == prefix) ? (1u << i) : 0u;
+          while (inm) {
+            const int i = __ffs(inm) - 1;
+            inm &= inm - 1;
+            uint32_t ui = su[0];
+#pragma unroll
+            for (int k2 = 1; k2 < 32; ++k2) ui = k2 == i ? su[k2] : ui;  // register select, no local memory
+            const int b = (int)((ui >> sh) & 31u);
+            const uint2 v = bins[b * 2 * BM + col];
+            bins[b * 2 * BM + col] = make_uint2(__float_as_uint(__uint_as_float(v.x) + __uint_as_float(ui)), v.y + 1u);
+          }
+          continue;
+        }
+        // pass 1 (every element): groups of G; duplicate bins inside a group are merged first, so
+        // the G read-modify-writes of a group hit distinct SMEM words and issue back to back
+        constexpr int G = 4;
+#pragma unroll
+        for (int i0 = 0; i0 < 32; i0 += G) {
+          int bk[G], cn[G];
+          float pm[G];
+#pragma unroll
+          for (int g = 0; g < G; ++g) {
+            const int b = bin_of(su[i0 + g]);
+            bk[g] = b >= 0 ? b : -1 - g;  // unique negative: no bin
+            pm[g] = b >= 0 ? __uint_as_float(su[i0 + g]) : 0.f;
+            cn[g] = b >= 0 ? 1 : 0;
+          }
+#pragma unroll
+          for (int g = 1; g < G; ++g)
+#pragma unroll
+            for (int h2 = 0; h2 < g; ++h2)
+              if (bk[h2] == bk[g]) {  // bk[h2] is the first occurrence (merged ones get -8 - g)
+                pm[h2] += pm[g];
+                cn[h2] += cn[g];
+                bk[g] = -8 - g;
+              }
+          uint2 v[G];
+#pragma unroll
+          for (int g = 0; g < G; ++g)
+            if (bk[g] >= 0) v[g] = bins[bk[g] * 2 * BM + col];
+#pragma unroll
+          for (int g = 0; g < G; ++g)
+            if (bk[g] >= 0)
+              bins[bk[g] * 2 * BM + col] = make_uint2(__float_as_uint(__uint_as_float(v[g].x) + pm[g]), v[g].y + cn[g]);
         }
       }
     }
@@ -186,21 +271,24 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         float cum = above;
         int cnt = above_n, cb = -1;
         for (int bi = NBIN - 1; bi >= 0; --bi) {
-          const float bm = bmass[bi * 2 * BM + col];
+          const uint2 bv = bins[bi * 2 * BM + col];
+          const float bm = __uint_as_float(bv.x);
           if (cum + bm >= T) { cb = bi; break; }
           cum += bm;
-          cnt += bcnt[bi * 2 * BM + col];
+          cnt += (int)bv.y;
         }
-        const float w = (hi - lo) / (float)NBIN;
         if (!last) {
           const int bsel = cb < 0 ? 0 : cb;
-          row_lo[ridx] = lo + bsel * w;
-          row_hi[ridx] = bsel == NBIN - 1 ? hi : lo + (bsel + 1) * w;
+          const uint32_t np = pass == 1 ? (uint32_t)(96 + bsel) << 23 : prefix | ((uint32_t)bsel << sh);
+          row_lo[ridx] = __uint_as_float(np);  // the next pass's prefix (bits)
+          row_am[ridx] = cum;  // mass / count of the bins above the chosen one (and above hi)
+          row_an[ridx] = cnt;
         } else {
           int need = 0;
           if (cb >= 0 && cum < T) {
-            const int bn_ = bcnt[cb * 2 * BM + col];
-            const float mean = bmass[cb * 2 * BM + col] / (float)max(bn_, 1);
+            const uint2 bv = bins[cb * 2 * BM + col];
+            const int bn_ = (int)bv.y;
+            const float mean = __uint_as_float(bv.x) / (float)max(bn_, 1);
             need = min(bn_, max(1, (int)ceilf((T - cum) / mean)));
           }
           counts[ridx] = max(1, cnt + need);
@@ -236,16 +324,16 @@ __global__ void __launch_bounds__(1024) k_density_reduce(int N, const int32_t* _
 }  // namespace dens
 
 cudaError_t launch_attention_density(const CUtensorMap* tm_q, const CUtensorMap* tm_k, int B, int H, int N, int d,
-                                     float scale, double tau, int passes, float* row_m, float* row_z, float* row_lo,
-                                     float* row_hi, int32_t* counts, double* density, cudaStream_t st) {
+                                     float scale, double tau, int passes, float* rs, size_t rows, int32_t* counts,
+                                     double* density, cudaStream_t st) {
   const float c = scale * 1.4426950408889634f;
   const dim3 grid((N + 2 * dens::BM - 1) / (2 * dens::BM), B * H);
   auto run = [&](auto kfn, int smem) -> cudaError_t {
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     for (int p = 0; p <= passes; ++p)
-      kfn<<<grid, dens::NTHREADS, smem, st>>>(*tm_q, *tm_k, H, N, c, p, p == passes ? 1 : 0, tau, row_m, row_z,
-                                             row_lo, row_hi, counts);
+      kfn<<<grid, dens::NTHREADS, smem, st>>>(*tm_q, *tm_k, H, N, c, p, p == passes ? 1 : 0, tau, rs, rows,
+                                             counts);
     return cudaGetLastError();
   };
   cudaError_t e = d == 128 ? run(dens::k_density<128>, dens::Smem<128>::ALLOC)
