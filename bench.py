@@ -424,7 +424,8 @@ def run_ours(args):
                      "traffic": traffic,
                      "algorithmic": "kept FLOPs 4*d*sum_a |Q_a| sum_{c in kept[a]} |K_c| per launch (rank 0)"},
         "layer_kept_tflops": f_kept_total / (ms * 1e-3) / 1e12,
-        "gpu_launches": pb.launches_per_layer(args.iters, bool(args.sel_flags & pb.CLUSTER_KMEANS)) * K,
+        "gpu_launches": pb.launches_per_layer(args.iters, bool(args.sel_flags & pb.CLUSTER_KMEANS), args.kq,
+                                              args.kk) * K,
         "clocks": clk, "e2e": e2e, "cpu_baseline": cpu, "clustering_reuse": reuse,
     }
     print(json.dumps(line), flush=True)

@@ -132,11 +132,16 @@ def _cuda(t: torch.Tensor, name: str):
         raise ValueError(f"{name} must be a CUDA tensor (no CPU fallback)")
 
 
-def launches_per_layer(iters: int, kmeans: bool = False) -> int:
+def launches_per_layer(iters: int, kmeans: bool = False, kq: int = 100, kk: int = 500) -> int:
     """Kernels the fused entry launches per layer: init_sample 1; per iteration and side: anchor
-    prep 2 (k-means: 1) + assign GEMM 1 + counting sort 3 + centroid update 1; selection 4 (Abar,
-    rows, count, emit); V permute 1; work list 1; attention 1."""
-    return 1 + iters * 2 * (6 if kmeans else 7) + 4 + 1 + 1 + 1
+    prep 2, + 1 partial-Gamma reduction when the anchor side has > 64 centroids (k-means: 1) +
+    assign GEMM 1 + counting sort 3 + centroid update 1; selection 4 (Abar, rows, count, emit);
+    V permute 1; work list 1; attention 1."""
+    if kmeans:
+        per_iter = 2 * 6
+    else:  # step A anchors on C_q (kq rows), step B on C_k (kk rows)
+        per_iter = 2 * 6 + 2 + (kq > 64) + (kk > 64)
+    return 1 + iters * per_iter + 4 + 1 + 1 + 1
 
 
 def workspace_bytes(B, H, N, d, kq, kk) -> int:
@@ -225,7 +230,7 @@ def coclust_permute(labels, k, ws=None):
     BH = labels.numel() // N
     perm = torch.empty_like(labels)
     offs = torch.empty(*labels.shape[:-1], k + 1, dtype=torch.int32, device=labels.device)
-    w, wn = _ws(ws, BH * ((N + 1023) // 1024) * k * 4 + 4096, labels.device)
+    w, wn = _ws(ws, BH * ((N + 1023) // 1024 + 1) * k * 4 + 4096, labels.device)
     _check(lib().coclust_permute(BH, N, k, _ptr(labels), _ptr(perm), _ptr(offs), w, wn,
                                  _stream(labels)))
     return perm, offs

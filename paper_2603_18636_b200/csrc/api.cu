@@ -68,9 +68,10 @@ struct AssignScratch {
 AssignScratch carve_assign(Carve& c, int BH, int N, int d, int kq, int kk) {
   AssignScratch s;
   const int kmax = std::max(kq, kk);
-  s.gamma = c.take<double>((size_t)BH * d * d);
+  // partial Gammas of the anchor-row splits (k_gamma): ceil(K_a / kGammaRows) slabs
+  s.gamma = c.take<double>((size_t)((kmax + kGammaRows - 1) / kGammaRows) * BH * d * d);
   s.wsplit = c.take<__nv_bfloat16>((size_t)BH * std::max(pad_k(kq), pad_k(kk)) * 2 * d);
-  s.hist = c.take<int32_t>((size_t)BH * ((N + kSortTile - 1) / kSortTile) * kmax);
+  s.hist = c.take<int32_t>((size_t)BH * ((N + kSortTile - 1) / kSortTile + 1) * kmax);  // + label sizes
   s.bias = c.take<float>((size_t)BH * std::max(pad_k(kq), pad_k(kk)));
   return s;
 }
@@ -421,10 +422,10 @@ cs_status coclust_permute(int BH, int N, int k, const int32_t* labels, int32_t* 
   if (N >= (1 << 24) || (long long)BH * N >= (1LL << 31)) return fail(CS_ERR_UNSUPPORTED, "too many tokens");
   CS_CHECK(check_k(k, 1 << 30, "k"));
   NEED(labels, "labels"); NEED(perm, "perm"); NEED(offs, "offs");
-  const size_t need = (size_t)BH * ((N + kSortTile - 1) / kSortTile) * k * 4 + 256;
+  const size_t need = (size_t)BH * ((N + kSortTile - 1) / kSortTile + 1) * k * 4 + 256;
   CS_CHECK(check_ws(ws, ws_bytes, need));
   Carve c(ws);
-  int32_t* hist = c.take<int32_t>((size_t)BH * ((N + kSortTile - 1) / kSortTile) * k);
+  int32_t* hist = c.take<int32_t>((size_t)BH * ((N + kSortTile - 1) / kSortTile + 1) * k);
   CS_CUDA(launch_csort(labels, BH, N, k, perm, offs, hist, static_cast<cudaStream_t>(stream)), "csort");
   return CS_OK;
 }

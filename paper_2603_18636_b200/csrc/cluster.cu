@@ -125,22 +125,28 @@ __global__ void __launch_bounds__(256) k_init_sample(XView q, XView k, int N, in
 template <int D>
 __global__ void __launch_bounds__(256) k_gamma(const float* __restrict__ ca, int ka,
                                                double* __restrict__ gamma) {
-  constexpr int CH = 32, TB = 64, NB = D / TB;
+  // split over the anchor rows: CTA z sums rows [z GR, (z+1) GR) into the partial Gamma_z (a
+  // [gridDim.z][BH][D][D] slab); k_gamma_reduce adds the partials into slab 0 in a fixed order.
+  // Short serial loops keep the kernel off the latency floor when few heads share a launch
+  // (head-parallel ranks).
+  constexpr int CH = 32, TB = 64, NB = D / TB, GR = kGammaRows;
   __shared__ __align__(16) double sa[CH][D];
   // upper-triangle block index -> (row block, column block), column block >= row block
   int rb = 0, cb = blockIdx.y;
   while (cb >= NB - rb) { cb -= NB - rb; ++rb; }
   cb += rb;
   const int bh = blockIdx.x, e0 = rb * TB, f0 = cb * TB;
+  const int r_beg = blockIdx.z * GR, r_end = min(ka, r_beg + GR);
   const float* A = ca + (size_t)bh * ka * D;
+  gamma += (size_t)blockIdx.z * gridDim.x * D * D;
   const int t = threadIdx.x, ti = t >> 4, tj = t & 15;
   double acc[4][4];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
-  for (int a0 = 0; a0 < ka; a0 += CH) {
-    const int n = min(CH, ka - a0);
+  for (int a0 = r_beg; a0 < r_end; a0 += CH) {
+    const int n = min(CH, r_end - a0);
     __syncthreads();
     for (int i = t; i < CH * D / 4; i += 256) {
       const int r = i / (D / 4), c = (i % (D / 4)) * 4;
@@ -169,6 +175,19 @@ __global__ void __launch_bounds__(256) k_gamma(const float* __restrict__ ca, int
 #pragma unroll
       for (int j = 0; j < 4; ++j) G[(size_t)(f0 + tj + 16 * j) * D + e0 + ti + 16 * i] = acc[i][j];
   }
+}
+
+// slab 0 += slabs 1 .. nparts-1 (fixed order: deterministic); grid ceil(BH D D / 2 / 256)
+__global__ void __launch_bounds__(256) k_gamma_reduce(double* __restrict__ gamma, size_t slab, int nparts) {
+  const size_t i = ((size_t)blockIdx.x * 256 + threadIdx.x) * 2;
+  if (i >= slab) return;
+  double2 a = *reinterpret_cast<const double2*>(gamma + i);
+  for (int z = 1; z < nparts; ++z) {
+    const double2 b = *reinterpret_cast<const double2*>(gamma + (size_t)z * slab + i);
+    a.x += b.x;
+    a.y += b.y;
+  }
+  *reinterpret_cast<double2*>(gamma + i) = a;
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -370,56 +389,95 @@ __global__ void __launch_bounds__(256) k_csort_hist(const int32_t* __restrict__ 
   for (int c = threadIdx.x; c < K; c += blockDim.x) H[c] = sh_hist[c];
 }
 
-// grid BH, block 1024 (K <= 1024): hist (counts) -> per-tile bases in place; offs.
-__global__ void __launch_bounds__(1024) k_csort_scan(int N, int K, int ntiles,
-                                                     int32_t* __restrict__ hist,
-                                                     int32_t* __restrict__ offs) {
-  __shared__ int sbuf[32];
-  const int bh = blockIdx.x, c = threadIdx.x;
+// grid (ceil(K / 32), BH), block 256 = 32 labels x 8 tile groups: hist (counts) -> per-tile bases
+// relative to the label's first position, in place; tot[bh][c] = label sizes.  The serial chains
+// are ceil(ntiles / 8) long (not ntiles), so the kernel stays short when few heads share a launch.
+__global__ void __launch_bounds__(256) k_csort_scan(int K, int ntiles, int32_t* __restrict__ hist,
+                                                    int32_t* __restrict__ tot) {
+  __shared__ int gs[8][33];
+  const int bh = blockIdx.y, cl = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + cl;
+  const int per = (ntiles + 7) / 8, t0 = g * per, t1 = min(ntiles, t0 + per);
   int32_t* H = hist + (size_t)bh * ntiles * K;
-  int tot = 0;
+  int sum = 0;
   if (c < K)
-    for (int t = 0; t < ntiles; ++t) tot += H[(size_t)t * K + c];
-  int start = block_exclusive_scan(tot, nullptr, sbuf);
+    for (int t = t0; t < t1; ++t) sum += H[(size_t)t * K + c];
+  gs[g][cl] = sum;
+  __syncthreads();
+  int base = 0;
+  for (int q = 0; q < g; ++q) base += gs[q][cl];
   if (c < K) {
-    offs[(size_t)bh * (K + 1) + c] = start;
-    int base = start;
-    for (int t = 0; t < ntiles; ++t) {
+    for (int t = t0; t < t1; ++t) {
       const int h = H[(size_t)t * K + c];
       H[(size_t)t * K + c] = base;
       base += h;
     }
+    if (g == 7) tot[(size_t)bh * K + c] = base;
   }
-  if (c == 0) offs[(size_t)bh * (K + 1) + K] = N;
 }
 
-// grid (ceil(ntiles/4), BH), block 128: one warp per tile, in token order.
-__global__ void __launch_bounds__(128) k_csort_scatter(const int32_t* __restrict__ lab, int N, int K,
+// grid (ntiles, BH), block 256 = 8 warps x 128 tokens of one tile, dyn smem 9 K ints.
+// Label starts = exclusive scan of tot (every CTA, K <= 1024; CTA 0 also writes offs); per-warp
+// label counts (match_any) -> per-warp cursors -> each warp scatters its tokens in order: stable.
+__global__ void __launch_bounds__(256) k_csort_scatter(const int32_t* __restrict__ lab, int N, int K,
                                                        int ntiles, const int32_t* __restrict__ base,
+                                                       const int32_t* __restrict__ tot,
+                                                       int32_t* __restrict__ offs,
                                                        int32_t* __restrict__ perm) {
-  extern __shared__ int sh_cnt[];  // [4][K]
-  const int bh = blockIdx.y, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int t = blockIdx.x * 4 + w;
-  if (t >= ntiles) return;
-  int* cnt = sh_cnt + w * K;
-  const int32_t* B0 = base + ((size_t)bh * ntiles + t) * K;
-  for (int c = lane; c < K; c += 32) cnt[c] = B0[c];
-  __syncwarp();
+  extern __shared__ int sh_cs[];
+  int* lstart = sh_cs;      // [K]
+  int* wc = sh_cs + K;      // [8][K]: per-warp counts, then per-warp cursors
+  __shared__ int sbuf[32];
+  const int bh = blockIdx.y, t = blockIdx.x, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // label starts
+  const int per = (K + 255) / 256, c0 = threadIdx.x * per, c1 = min(K, c0 + per);
+  const int32_t* T = tot + (size_t)bh * K;
+  int loc = 0;
+  for (int c = c0; c < c1; ++c) loc += T[c];
+  int run = block_exclusive_scan(loc, nullptr, sbuf);
+  for (int c = c0; c < c1; ++c) {
+    lstart[c] = run;
+    if (t == 0) offs[(size_t)bh * (K + 1) + c] = run;
+    run += T[c];
+  }
+  if (t == 0 && threadIdx.x == 0) offs[(size_t)bh * (K + 1) + K] = N;
+  for (int i = threadIdx.x; i < 8 * K; i += 256) wc[i] = 0;
+  __syncthreads();
   const int32_t* L = lab + (size_t)bh * N;
-  int32_t* P = perm + (size_t)bh * N;
-  const int i0 = t * kSortTile, i1 = min(N, i0 + kSortTile);
+  const int i0 = t * kSortTile + w * (kSortTile / 8), i1 = min(N, i0 + kSortTile / 8);
   const unsigned lt = (1u << lane) - 1u;
+  int* cw = wc + w * K;
+  for (int i = i0; i < i1; i += 32) {  // per-warp label counts
+    const int me = i + lane;
+    const bool valid = me < i1;
+    const int l = valid ? L[me] : -1 - lane;
+    const unsigned peers = __match_any_sync(0xffffffffu, l);
+    if (valid && __popc(peers & lt) == 0) cw[l] += __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  const int32_t* B0 = base + ((size_t)bh * ntiles + t) * K;
+  for (int c = threadIdx.x; c < K; c += 256) {  // counts -> cursors
+    int cur = lstart[c] + B0[c];
+    for (int q = 0; q < 8; ++q) {
+      const int n = wc[q * K + c];
+      wc[q * K + c] = cur;
+      cur += n;
+    }
+  }
+  __syncthreads();
+  int32_t* P = perm + (size_t)bh * N;
   for (int i = i0; i < i1; i += 32) {
     const int me = i + lane;
     const bool valid = me < i1;
     const int l = valid ? L[me] : -1 - lane;  // unique dummy keys for the tail
     const unsigned peers = __match_any_sync(0xffffffffu, l);
     const int rank = __popc(peers & lt);
-    const int basep = valid ? cnt[l] : 0;
+    const int basep = valid ? cw[l] : 0;
     __syncwarp();
     if (valid) {
       P[basep + rank] = me;
-      if (rank == 0) cnt[l] = basep + __popc(peers);
+      if (rank == 0) cw[l] = basep + __popc(peers);
     }
     __syncwarp();
   }
@@ -462,14 +520,18 @@ cudaError_t launch_init_sample(XView q, XView k, int BH, int N, int d, int kq, i
 
 cudaError_t launch_anchor_prep(const float* ca, int ka, const float* cself, int ks, int ks_pad,
                                int BH, int d, double* gamma, __nv_bfloat16* wsplit, cudaStream_t st) {
+  const int nparts = (ka + kGammaRows - 1) / kGammaRows;  // gamma holds nparts x BH x d x d
+  const size_t slab = (size_t)BH * d * d;
   if (d == 128) {
     constexpr int smem = 2 * 32 * 128 * 8;
     cudaError_t e = cudaFuncSetAttribute(k_anchor_w<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    k_gamma<128><<<dim3(BH, 3), 256, 0, st>>>(ca, ka, gamma);
+    k_gamma<128><<<dim3(BH, 3, nparts), 256, 0, st>>>(ca, ka, gamma);
+    if (nparts > 1) k_gamma_reduce<<<(unsigned)((slab / 2 + 255) / 256), 256, 0, st>>>(gamma, slab, nparts);
     k_anchor_w<128><<<dim3((ks_pad + 31) / 32, BH), 256, smem, st>>>(cself, ks, ks_pad, gamma, wsplit);
   } else {
-    k_gamma<64><<<dim3(BH, 1), 256, 0, st>>>(ca, ka, gamma);
+    k_gamma<64><<<dim3(BH, 1, nparts), 256, 0, st>>>(ca, ka, gamma);
+    if (nparts > 1) k_gamma_reduce<<<(unsigned)((slab / 2 + 255) / 256), 256, 0, st>>>(gamma, slab, nparts);
     k_anchor_w<64><<<dim3((ks_pad + 31) / 32, BH), 256, 2 * 32 * 64 * 8, st>>>(cself, ks, ks_pad, gamma, wsplit);
   }
   return cudaGetLastError();
@@ -492,10 +554,10 @@ cudaError_t launch_seg_mean(XView x, int BH, int N, int d, int K, const int32_t*
 cudaError_t launch_csort(const int32_t* lab, int BH, int N, int K, int32_t* perm, int32_t* offs,
                          int32_t* hist, cudaStream_t st) {
   const int ntiles = (N + kSortTile - 1) / kSortTile;
+  int32_t* tot = hist + (size_t)BH * ntiles * K;  // label sizes [BH][K] after the tile histograms
   k_csort_hist<<<dim3(ntiles, BH), 256, K * sizeof(int), st>>>(lab, N, K, ntiles, hist);
-  k_csort_scan<<<BH, 1024, 0, st>>>(N, K, ntiles, hist, offs);
-  k_csort_scatter<<<dim3((ntiles + 3) / 4, BH), 128, 4 * K * sizeof(int), st>>>(lab, N, K, ntiles,
-                                                                               hist, perm);
+  k_csort_scan<<<dim3((K + 31) / 32, BH), 256, 0, st>>>(K, ntiles, hist, tot);
+  k_csort_scatter<<<dim3(ntiles, BH), 256, 9 * K * sizeof(int), st>>>(lab, N, K, ntiles, hist, tot, offs, perm);
   return cudaGetLastError();
 }
 

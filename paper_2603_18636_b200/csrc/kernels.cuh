@@ -13,6 +13,7 @@ namespace cs {
 
 constexpr int kSortTile = 1024;  // tokens per counting-sort tile
 constexpr int kMaxClusters = 1024;
+constexpr int kGammaRows = 64;   // anchor rows per partial Gamma (k_gamma split over C_a rows)
 
 // Strided bf16 [B, H, N, d] view (d contiguous).
 struct XView {

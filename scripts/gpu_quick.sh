@@ -6,4 +6,4 @@ timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e --r
 python -c "
 import json; d=json.load(open('gpurun_out/bench_q.json')); s=d['stages_ms']; print('ms %.3f' % d['value'], s, 'frac %.4f' % d['roofline']['frac'], d['clocks'])"
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:k_ --csv --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --reuse-steps 0 > /dev/null 2>&1; echo "ncu launches rc=$?"
-python scripts/launch_summary.py gpurun_out/launches.csv 36 "" 2
+python scripts/launch_summary.py gpurun_out/launches.csv 40 "" 2

@@ -126,6 +126,50 @@ def run_cells(a):
               f"{r['clustering_share']:.3f} |")
 
 
+def run_heads(a):
+    """Head-parallel scaling on one GPU: the layer of rank 0 at P = 1, 2, 4, 8 (its H / P heads,
+    global sampler keys), i.e. the per-rank work of BASELINE configs[2] without the other ranks.
+    Head-parallel has no collective on the data path, so the P-GPU layer time is the max over
+    ranks of these per-rank times (ranks differ only by their heads' budgets / cluster sizes)."""
+    dev = torch.device("cuda", 0)
+    c = CONFIGS["wan14b_720p"]
+    w = video_qkv(c["T"], c["Hs"], c["Ws"], c["H"], c["d"], seed=a.seed, device=dev)
+    H = c["H"]
+    ws = pb.Workspace()
+    rows = []
+    fout = open(a.out, "w") if a.out else None
+    base = None
+    for P in (1, 2, 4, 8):
+        Hl = H // P
+        times = []
+        for r in range(P) if a.all_ranks else range(1):
+            sl = slice(r * Hl, (r + 1) * Hl)
+            q, k, v = (t[:, sl].contiguous() for t in (w.q, w.k, w.v))
+            out = torch.empty_like(q)
+            budget = torch.full((Hl,), 0.2, dtype=torch.float32, device=dev)
+            for _ in range(a.warmup):
+                pb.coclust_sparse_attention(q, k, v, c["kq"], c["kk"], c["iters"], budget, seed=a.seed,
+                                            rule=RULES["fixed"], out=out, ws=ws, head_offset=r * Hl, heads_total=H)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record()
+            for _ in range(a.steps):
+                pb.coclust_sparse_attention(q, k, v, c["kq"], c["kk"], c["iters"], budget, seed=a.seed,
+                                            rule=RULES["fixed"], out=out, ws=ws, head_offset=r * Hl, heads_total=H)
+            e1.record()
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1) / a.steps)
+            del q, k, v, out
+        t = max(times)
+        base = base or t
+        row = {"P": P, "heads_per_rank": Hl, "ms_per_rank_max": t, "ms_per_rank": times,
+               "predicted_scaling_efficiency": base / (P * t)}
+        rows.append(row)
+        print(json.dumps(row), flush=True)
+        if fout:
+            fout.write(json.dumps(row) + "\n")
+
+
 def run_layers(a):
     dev = torch.device("cuda", 0)
     c = CONFIGS[a.config]
@@ -177,7 +221,8 @@ def run_layers(a):
 def main():
     from bench import ClockSampler
     ap = argparse.ArgumentParser()
-    ap.add_argument("mode", choices=["cells", "layers"])
+    ap.add_argument("mode", choices=["cells", "layers", "heads"])
+    ap.add_argument("--all-ranks", action="store_true", help="heads mode: time every rank's shard")
     ap.add_argument("--config", default="wan1.3b_480p")
     ap.add_argument("--layers", type=int, default=30)
     ap.add_argument("--iters", type=int, default=2)
@@ -194,7 +239,7 @@ def main():
     t0 = time.time()
     clk = ClockSampler(0)
     clk.start()
-    (run_cells if a.mode == "cells" else run_layers)(a)
+    {"cells": run_cells, "layers": run_layers, "heads": run_heads}[a.mode](a)
     c = clk.stop()
     print(json.dumps({"clocks": c}), flush=True)
     if a.out:
