@@ -98,19 +98,31 @@ __global__ void __launch_bounds__(256) k_init_sample(XView q, XView k, int N, in
     }
   }
   __syncthreads();
-  // C^(0)[j] = X[idx[j]]  (bf16 -> fp32): 8 bf16 (16 B) per thread and load
+  // C^(0)[j] = X[idx[j]]  (bf16 -> fp32): 8 bf16 (16 B) per thread and load; 4 independent loads
+  // in flight per thread before the converts / stores (one launch per layer: latency matters)
   const int b = bh / X.H, h = bh % X.H;
   const int vpr = d / 8;  // 16-byte vectors per row
-  for (int e = threadIdx.x; e < K * vpr; e += blockDim.x) {
-    const int j = e / vpr, c = (e % vpr) * 8;
-    const uint4 v = *reinterpret_cast<const uint4*>(X.row(b, h, idx[j]) + c);
-    const __nv_bfloat16* pv = reinterpret_cast<const __nv_bfloat16*>(&v);
-    float4 lo, hi;
-    lo.x = __bfloat162float(pv[0]); lo.y = __bfloat162float(pv[1]); lo.z = __bfloat162float(pv[2]); lo.w = __bfloat162float(pv[3]);
-    hi.x = __bfloat162float(pv[4]); hi.y = __bfloat162float(pv[5]); hi.z = __bfloat162float(pv[6]); hi.w = __bfloat162float(pv[7]);
-    float4* dst = reinterpret_cast<float4*>(C + (size_t)j * d + c);
-    dst[0] = lo;
-    dst[1] = hi;
+  const int total = K * vpr;
+  for (int e0 = threadIdx.x; e0 < total; e0 += 4 * blockDim.x) {
+    uint4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = e0 + u * blockDim.x;
+      if (e < total) v[u] = *reinterpret_cast<const uint4*>(X.row(b, h, idx[e / vpr]) + (e % vpr) * 8);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = e0 + u * blockDim.x;
+      if (e >= total) break;
+      const int j = e / vpr, c = (e % vpr) * 8;
+      const __nv_bfloat16* pv = reinterpret_cast<const __nv_bfloat16*>(&v[u]);
+      float4 lo, hi;
+      lo.x = __bfloat162float(pv[0]); lo.y = __bfloat162float(pv[1]); lo.z = __bfloat162float(pv[2]); lo.w = __bfloat162float(pv[3]);
+      hi.x = __bfloat162float(pv[4]); hi.y = __bfloat162float(pv[5]); hi.z = __bfloat162float(pv[6]); hi.w = __bfloat162float(pv[7]);
+      float4* dst = reinterpret_cast<float4*>(C + (size_t)j * d + c);
+      dst[0] = lo;
+      dst[1] = hi;
+    }
   }
 }
 
