@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--ulysses-return", choices=["fused", "nccl"], default="fused",
                     help="Ulysses output path: attention epilogue stores into the owners' token blocks "
                          "(fused, CUDA IPC / NVLink) or NCCL all_to_all + unpack")
+    ap.add_argument("--graph", choices=["on", "off"], default="on",
+                    help="time the layer as CUDA-graph replays (one captured layer call; head-parallel)")
     ap.add_argument("--cpu-sample-rows", type=int, default=1500,
                     help="query rows of the oracle attention sample")
     return ap.parse_args()
@@ -279,10 +281,14 @@ def run_ours(args):
     for e in (x for row in evs for x in row):
         e.record()  # torch creates the CUDA event lazily, on first record
     torch.cuda.synchronize()
+    # stage times: an eager pass of K steps with the library's stage events (CUDA cannot time events
+    # recorded inside graph replays); with --graph off this pass is also the timed region
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    use_graph = args.graph == "on" and mode == "head"
     clocks = ClockSampler(local)
-    clocks.start()
-    time.sleep(0.3)
+    if not use_graph:
+        clocks.start()
+        time.sleep(0.3)
     torch.cuda.synchronize()
     t_start.record()
     step_starts = []
@@ -293,12 +299,39 @@ def run_ours(args):
         step(evs[i])
     t_end.record()
     torch.cuda.synchronize()
-    clk = clocks.stop()
     ms = t_start.elapsed_time(t_end) / K
     st_cluster = sum(step_starts[i].elapsed_time(evs[i][0]) for i in range(K)) / K
     st_select = sum(evs[i][0].elapsed_time(evs[i][1]) for i in range(K)) / K
     st_prep = sum(evs[i][1].elapsed_time(evs[i][2]) for i in range(K)) / K
     t_attn = sum(evs[i][2].elapsed_time(evs[i][3]) for i in range(K)) / K
+    ms_eager = ms
+    if use_graph:
+        # the timed region: K replays of one captured layer call (40 kernel launches become one
+        # graph launch; same kernels, same buffers, same bits)
+        cs = torch.cuda.Stream()
+        cs.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(cs):
+            step()
+        torch.cuda.current_stream().wait_stream(cs)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step()
+        for _ in range(max(args.warmup, 1)):
+            graph.replay()
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        clocks.start()
+        time.sleep(0.3)
+        torch.cuda.synchronize()
+        t_start.record()
+        for _ in range(K):
+            graph.replay()
+        t_end.record()
+        torch.cuda.synchronize()
+        ms = t_start.elapsed_time(t_end) / K
+    clk = clocks.stop()
     if world > 1:
         tt = torch.tensor([ms, t_attn], device=dev)
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
@@ -417,7 +450,9 @@ def run_ours(args):
         "kept_tflop_per_layer": f_kept_total / 1e12,
         "kept_frac": f_kept_total / dense_flops,
         "stages_ms": {"cocluster": st_cluster, "select": st_select, "permute_v_worklist": st_prep,
-                      "attention": t_attn},
+                      "attention": t_attn, "source": "eager pass with stage events" if use_graph else "timed region",
+                      "layer_eager": ms_eager},
+        "timing": "CUDA-graph replays of the layer" if use_graph else "eager calls",
         "roofline": {"kernel": "k_bsa_fwd", "bound": "tensor", "achieved": achieved, "peak": peak_sust,
                      "unit": "TFLOP/s", "frac": achieved / peak_sust, "frac_of_burst": achieved / peak_burst,
                      "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside a long step)",

@@ -150,12 +150,21 @@ def run_heads(a):
             for _ in range(a.warmup):
                 pb.coclust_sparse_attention(q, k, v, c["kq"], c["kk"], c["iters"], budget, seed=a.seed,
                                             rule=RULES["fixed"], out=out, ws=ws, head_offset=r * Hl, heads_total=H)
+            call = lambda: pb.coclust_sparse_attention(q, k, v, c["kq"], c["kk"], c["iters"], budget, seed=a.seed,
+                                                       rule=RULES["fixed"], out=out, ws=ws, head_offset=r * Hl,
+                                                       heads_total=H)
+            if a.graph:
+                torch.cuda.synchronize()
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    call()
+                call = g.replay
+                call()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             torch.cuda.synchronize()
             e0.record()
             for _ in range(a.steps):
-                pb.coclust_sparse_attention(q, k, v, c["kq"], c["kk"], c["iters"], budget, seed=a.seed,
-                                            rule=RULES["fixed"], out=out, ws=ws, head_offset=r * Hl, heads_total=H)
+                call()
             e1.record()
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1) / a.steps)
@@ -223,6 +232,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("mode", choices=["cells", "layers", "heads"])
     ap.add_argument("--all-ranks", action="store_true", help="heads mode: time every rank's shard")
+    ap.add_argument("--graph", action="store_true", help="heads mode: time CUDA-graph replays of the layer")
     ap.add_argument("--config", default="wan1.3b_480p")
     ap.add_argument("--layers", type=int, default=30)
     ap.add_argument("--iters", type=int, default=2)
