@@ -28,10 +28,26 @@ namespace attn {
 #ifdef CS_ATTN_DEBUG
 // event trace of one CTA (blockIdx 0,0): t[event][tile] = clock64 (debug variant only)
 __device__ long long g_trace[20][4096];
+// per-CTA timeline (debug variant): [cta][0] entry globaltimer, [1] after setup, [2] first S seen,
+// [3] exit, [4] smid, [5] nt
+__device__ long long g_cta[65536][6];
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ int smid() {
+  int s;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(s));
+  return s;
+}
+#define CS_CTA(e, v) \
+  if (threadIdx.x == 0 && blockIdx.y * gridDim.x + blockIdx.x < 65536) g_cta[blockIdx.y * gridDim.x + blockIdx.x][e] = (v)
 #define CS_TRACE(e, j) \
   if (blockIdx.x == 0 && blockIdx.y == 0 && (threadIdx.x & 31) == 0 && (j) < 4096) g_trace[e][j] = clock64()
 #else
 #define CS_TRACE(e, j)
+#define CS_CTA(e, v)
 #endif
 
 constexpr int BM = 128, BN = 128, UNIT = 8, UPT = BN / UNIT, NST = 2;
@@ -93,6 +109,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   int* ucum = reinterpret_cast<int*>(sm + L::OFF_UCUM);
   float* xch = reinterpret_cast<float*>(sm + L::OFF_XCH);
 
+  CS_CTA(0, gtimer());
   const int bh = blockIdx.y;
   const int item = blockIdx.x;
   const int32_t* ist = item_start + (size_t)bh * (kq + 1);
@@ -114,41 +131,62 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const bool split = !has1;
   const int warp = warp_id(), lane = lane_id();
 
-  // ---- setup: barriers (thread 0), TMEM (warp 9), unit table (warp 8)
-  if (threadIdx.x == 0) {
-    mbar_init(q_full, 1);
-    for (int s = 0; s < NST; ++s) {
-      mbar_init(k_full + s, 1); mbar_init(k_empty + s, 1);
-      mbar_init(v_full + s, 1); mbar_init(v_empty + s, 1);
+  // ---- setup: barriers + Q load (warp 8, lane 0: the Q tiles do not depend on the unit table, so
+  // their TMA is in flight while the table is built), TMEM (warp 9), unit table (warp 8)
+  if (warp == WARP_PRODUCER) {
+    if (lane == 0) {
+      mbar_init(q_full, 1);
+      for (int s = 0; s < NST; ++s) {
+        mbar_init(k_full + s, 1); mbar_init(k_empty + s, 1);
+        mbar_init(v_full + s, 1); mbar_init(v_empty + s, 1);
+      }
+      for (int t = 0; t < 2; ++t) mbar_init(s_full + t, 1);
+      for (int t = 0; t < 4; ++t) mbar_init(p_full + t, 128);
+      mbar_init(o_full, 1);
+      fence_barrier_init();
+      tma_prefetch_desc(&tm_q);
+      const int ntq = has1 ? 2 : 1;
+      mbar_arrive_expect_tx(q_full, ntq * L::QT);
+      for (int tq = 0; tq < ntq; ++tq)
+        for (int hf = 0; hf < L::HALVES; ++hf)
+          tma_load_2d(sm + L::OFF_Q + tq * L::QT + hf * L::HALF_Q, &tm_q, hf * 64,
+                      bh * N + qbeg + (t0 + tq) * BM, q_full);
     }
-    for (int t = 0; t < 2; ++t) mbar_init(s_full + t, 1);
-    for (int t = 0; t < 4; ++t) mbar_init(p_full + t, 128);
-    mbar_init(o_full, 1);
-    fence_barrier_init();
+    if (lane < 5) { tma_prefetch_desc(&kv.k[lane]); tma_prefetch_desc(&kv.v[lane]); }
   }
   if (warp == WARP_MMA) tmem_alloc(reinterpret_cast<uint32_t*>(misc), 512);
   if (warp == WARP_PRODUCER) {
-    tma_prefetch_desc(&tm_q);
-    if (lane < 5) { tma_prefetch_desc(&kv.k[lane]); tma_prefetch_desc(&kv.v[lane]); }
     const int n = n_rows ? n_rows[(size_t)bh * kq + a] : n_keep[bh];  // per-row counts (R11b)
     const int32_t* kl = kept + ((size_t)bh * kq + a) * kk;
     const int32_t* ok = offs_k + (size_t)bh * (kk + 1);
     int carry = 0;
-    for (int i0 = 0; i0 < n; i0 += 32) {
-      const int i = i0 + lane;
-      int nu = 0;
-      if (i < n) {
-        const int c = kl[i];
-        const int st = ok[c];
-        const int len = ok[c + 1] - st;
-        kstart[i] = st; klen[i] = len;
-        nu = (len + UNIT - 1) / UNIT;
-      }
-      int x = nu;
+    // 4 chunks of 32 kept clusters per round: all kept-list loads, then all offset loads, in
+    // flight together (two dependent global-load rounds per 128 clusters)
+    for (int i0 = 0; i0 < n; i0 += 128) {
+      int c4[4], st4[4], en4[4];
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) { int y = __shfl_up_sync(0xffffffffu, x, o); if (lane >= o) x += y; }
-      if (i < n) ucum[i] = carry + x - nu;
-      carry += __shfl_sync(0xffffffffu, x, 31);
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + 32 * u + lane;
+        c4[u] = i < n ? kl[i] : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + 32 * u + lane;
+        st4[u] = i < n ? ok[c4[u]] : 0;
+        en4[u] = i < n ? ok[c4[u] + 1] : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + 32 * u + lane;
+        const int len = en4[u] - st4[u];
+        const int nu = i < n ? (len + UNIT - 1) / UNIT : 0;
+        if (i < n) { kstart[i] = st4[u]; klen[i] = len; }
+        int x = nu;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) { int y = __shfl_up_sync(0xffffffffu, x, o); if (lane >= o) x += y; }
+        if (i < n) ucum[i] = carry + x - nu;
+        carry += __shfl_sync(0xffffffffu, x, 31);
+      }
     }
     if (lane == 0) { ucum[n] = carry; misc[1] = carry; misc[2] = n; }
   }
@@ -159,18 +197,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const int U = misc[1];
   const int nkeep = misc[2];
   const int nt = (U + UPT - 1) / UPT;
+  CS_CTA(1, gtimer());
+  CS_CTA(4, smid());
+  CS_CTA(5, nt | (split ? (1 << 20) : 0));
 
   if (warp == WARP_PRODUCER || warp == WARP_VLOAD) {
     // ================= TMA producers: warp 8 -> Q and K(j), warp 10 -> V(j) =================
     const bool is_v = warp == WARP_VLOAD;
-    if (!is_v && lane == 0) {
-      const int ntq = has1 ? 2 : 1;
-      mbar_arrive_expect_tx(q_full, ntq * L::QT);
-      for (int tq = 0; tq < ntq; ++tq)
-        for (int hf = 0; hf < L::HALVES; ++hf)
-          tma_load_2d(sm + L::OFF_Q + tq * L::QT + hf * L::HALF_Q, &tm_q, hf * 64,
-                      bh * N + qbeg + (t0 + tq) * BM, q_full);
-    }
     // Unit rows of tile jj, computed by lanes 0..UPT-1 (lane u <-> unit u of the tile) with a
     // cursor over the kept clusters (clusters are visited in order: usually 0-1 steps).
     int cur = 0;  // kept-cluster index of the first unit of the current tile (warp-uniform)
@@ -395,6 +428,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       for (int j = 0; j < my_nt; ++j) {
         mbar_wait(s_full + tq, j & 1);
         CS_TRACE(5 + 2 * tq, j);
+        if (j == 0 && warp == 0) CS_CTA(2, gtimer());
         tc_fence_after();
         uint32_t su[BN];
 #pragma unroll
@@ -551,11 +585,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
+  CS_CTA(3, gtimer());
 }
 
 }  // namespace attn
 
 #ifdef CS_ATTN_DEBUG
+extern "C" int cs_debug_attn_cta(void* host, size_t bytes) {
+  return (int)cudaMemcpyFromSymbol(host, attn::g_cta, bytes < sizeof(attn::g_cta) ? bytes : sizeof(attn::g_cta));
+}
 extern "C" int cs_debug_attn_trace(void* host, size_t bytes) {
   return (int)cudaMemcpyFromSymbol(host, attn::g_trace, bytes < sizeof(attn::g_trace) ? bytes : sizeof(attn::g_trace));
 }

@@ -1,0 +1,3 @@
+mkdir -p gpurun_out
+CS_VARIANT=dbg CS_EXTRA_FLAGS="-DCS_ATTN_DEBUG" python -m paper_2603_18636_b200.build > gpurun_out/build2.log 2>&1 || { cat gpurun_out/build2.log; exit 1; }
+COCLUST_LIB=paper_2603_18636_b200/libcoclust_dbg.so H=${H:-8} timeout 300 python scripts/dbg_cta_timeline.py 2>&1 | tail -12
