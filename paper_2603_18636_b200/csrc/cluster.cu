@@ -551,10 +551,13 @@ cudaError_t launch_anchor_prep(const float* ca, int ka, const float* cself, int 
 
 cudaError_t launch_seg_mean(XView x, int BH, int N, int d, int K, const int32_t* perm,
                             const int32_t* offs, float* C, __nv_bfloat16* xperm, cudaStream_t st) {
-  // warps per cluster: about one warp per 64 mean members, a power of two in [1, 8]
+  // warps per cluster: about one warp per CS_SEG_ROWS mean members, a power of two in [1, 8]
+#ifndef CS_SEG_ROWS
+#define CS_SEG_ROWS 64
+#endif
   const int mean = N / K;
   int nwc = 1;
-  while (nwc < 8 && nwc * 64 < mean) nwc <<= 1;
+  while (nwc < 8 && nwc * CS_SEG_ROWS < mean) nwc <<= 1;
   const dim3 grid((K + 8 / nwc - 1) / (8 / nwc), BH);
   if (d == 128)
     k_seg_mean<128><<<grid, 256, 0, st>>>(x, N, K, nwc, perm, offs, C, xperm);
