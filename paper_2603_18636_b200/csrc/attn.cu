@@ -30,7 +30,7 @@ namespace attn {
 __device__ long long g_trace[20][4096];
 // per-CTA timeline (debug variant): [cta][0] entry globaltimer, [1] after setup, [2] first S seen,
 // [3] exit, [4] smid, [5] nt
-__device__ long long g_cta[65536][6];
+__device__ long long g_cta[65536][8];
 __device__ __forceinline__ long long gtimer() {
   long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -43,11 +43,14 @@ __device__ __forceinline__ int smid() {
 }
 #define CS_CTA(e, v) \
   if (threadIdx.x == 0 && blockIdx.y * gridDim.x + blockIdx.x < 65536) g_cta[blockIdx.y * gridDim.x + blockIdx.x][e] = (v)
+#define CS_CTA_W(e, v) \
+  if ((threadIdx.x & 31) == 0 && blockIdx.y * gridDim.x + blockIdx.x < 65536) g_cta[blockIdx.y * gridDim.x + blockIdx.x][e] = (v)
 #define CS_TRACE(e, j) \
   if (blockIdx.x == 0 && blockIdx.y == 0 && (threadIdx.x & 31) == 0 && (j) < 4096) g_trace[e][j] = clock64()
 #else
 #define CS_TRACE(e, j)
 #define CS_CTA(e, v)
+#define CS_CTA_W(e, v)
 #endif
 
 constexpr int BM = 128, BN = 128, UNIT = 8, UPT = BN / UNIT, NST = 2;
@@ -154,7 +157,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     if (lane < 5) { tma_prefetch_desc(&kv.k[lane]); tma_prefetch_desc(&kv.v[lane]); }
   }
-  if (warp == WARP_MMA) tmem_alloc(reinterpret_cast<uint32_t*>(misc), 512);
+  if (warp == WARP_MMA) {
+    tmem_alloc(reinterpret_cast<uint32_t*>(misc), 512);
+    CS_CTA_W(6, gtimer());  // TMEM allocated
+  }
   if (warp == WARP_PRODUCER) {
     const int n = n_rows ? n_rows[(size_t)bh * kq + a] : n_keep[bh];  // per-row counts (R11b)
     const int32_t* kl = kept + ((size_t)bh * kq + a) * kk;
@@ -189,6 +195,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
     }
     if (lane == 0) { ucum[n] = carry; misc[1] = carry; misc[2] = n; }
+    CS_CTA_W(7, gtimer());  // unit table built
   }
   tc_fence_before();
   __syncthreads();

@@ -11,7 +11,7 @@ budget = torch.full((H,), 0.2, device='cuda')
 for _ in range(2):
     o = pb.coclust_sparse_attention(w.q, w.k, w.v, 100, 500, 2, budget, rule=pb.RULE_FIXED)
 torch.cuda.synchronize()
-buf = np.zeros((65536, 6), np.int64)
+buf = np.zeros((65536, 8), np.int64)
 pb.lib().cs_debug_attn_cta(buf.ctypes.data_as(ctypes.c_void_p), ctypes.c_size_t(buf.nbytes))
 v = buf[buf[:, 3] > 0]
 t0 = v[:, 0].min()
@@ -22,6 +22,8 @@ first = (v[:, 2] - v[:, 1]) / 1e3
 print("CTA duration us: median %.1f  mean %.1f" % (np.median(dur), dur.mean()))
 print("setup (entry -> tables/TMEM ready) us: median %.2f mean %.2f" % (np.median(setup), setup.mean()))
 print("ready -> first S tile us: median %.2f mean %.2f" % (np.median(first), first.mean()))
+print("  entry -> TMEM allocated us: median %.2f; entry -> unit table built us: median %.2f" %
+      (np.median((v[:, 6] - v[:, 0]) / 1e3), np.median((v[:, 7] - v[:, 0]) / 1e3)))
 nt = v[:, 5] & 0xfffff
 sp = (v[:, 5] >> 20) & 1
 loop = dur - setup - first
