@@ -74,13 +74,54 @@ __global__ void __launch_bounds__(256) k_init_sample(XView q, XView k, int N, in
       idx[i] = (int)(z % (unsigned long long)(N - K + i + 1));
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      for (int i = 0; i < K; ++i) {
-        const int j = N - K + i, t = idx[i];
-        const int pick = ((sm_bits[t >> 5] >> (t & 31)) & 1u) ? j : t;
-        sm_bits[pick >> 5] |= 1u << (pick & 31);
+    // Floyd's insertions, resolved in parallel (identical picks): with j_i = N - K + i,
+    //  - t_i < N - K: t_i was picked before iff an earlier draw has the same value (the first
+    //    occurrence of a value below N - K is always picked), so pick_i = dup ? j_i : t_i;
+    //  - t_i == j_i: never picked before -> pick_i = t_i;
+    //  - N - K <= t_i < j_i (t_i = j_m, m < i; about K^2 / 2N draws): j_m was picked before iff
+    //    pick_m == j_m or an earlier draw t_k == j_m (m <= k < i) was picked as itself; resolved by
+    //    one thread in increasing i over just these draws.
+    int* pick = idx + K;            // [K]
+    uint32_t* caseb = reinterpret_cast<uint32_t*>(pick + K);  // [32] bitmap of the third case
+    const int NK = N - K;
+    for (int w = threadIdx.x; w < 32; w += blockDim.x) caseb[w] = 0u;
+    __syncthreads();
+    for (int i = threadIdx.x; i < K; i += blockDim.x) {
+      const int t = idx[i];
+      if (t < NK) {
+        bool dup = false;
+        for (int k2 = 0; k2 < i && !dup; ++k2) dup = idx[k2] == t;
+        pick[i] = dup ? NK + i : t;
+      } else if (t == NK + i) {
+        pick[i] = t;
+      } else {
+        pick[i] = -1;
+        atomicOr(&caseb[i >> 5], 1u << (i & 31));
       }
     }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 0; w < 32; ++w) {
+        uint32_t mb = caseb[w];
+        while (mb) {
+          const int i = (w << 5) + __ffs(mb) - 1;
+          mb &= mb - 1;
+          const int t = idx[i], m = t - NK;
+          bool taken = pick[m] == t;  // j_m picked at step m
+          for (int w2 = m >> 5; w2 <= (i >> 5) && !taken; ++w2) {  // earlier third-case draws == j_m
+            uint32_t mk = caseb[w2];
+            while (mk && !taken) {
+              const int k2 = (w2 << 5) + __ffs(mk) - 1;
+              mk &= mk - 1;
+              if (k2 >= m && k2 < i && idx[k2] == t && pick[k2] == t) taken = true;
+            }
+          }
+          pick[i] = taken ? NK + i : t;
+        }
+      }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < K; i += blockDim.x) atomicOr(&sm_bits[pick[i] >> 5], 1u << (pick[i] & 31));
     __syncthreads();
     // ascending compaction of the bitmap: each thread owns a contiguous word range
     const int per = (nwords + blockDim.x - 1) / blockDim.x;
@@ -519,7 +560,7 @@ __global__ void __launch_bounds__(256) k_permute_rows(XView x, int N, int d,
 cudaError_t launch_init_sample(XView q, XView k, int BH, int N, int d, int kq, int kk,
                                unsigned long long seed, int h_off, int h_tot, const int32_t* init_q,
                                const int32_t* init_k, float* cq, float* ck, cudaStream_t st) {
-  const size_t smem = (size_t)((N + 31) / 32) * 4 + (size_t)max(kq, kk) * 4;
+  const size_t smem = (size_t)((N + 31) / 32) * 4 + (size_t)max(kq, kk) * 8 + 32 * 4;  // bitmap, draws, picks, flags
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k_init_sample, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);

@@ -409,14 +409,17 @@ def test_fused_toy_end_to_end(pb):
         pytest.skip(f"toy seed has a near-tie (min gap {min_gap:.2e}); teacher-forced tests cover it")
 
 
-def test_sampler_matches_oracle_via_explicit_init(pb):
-    """coclust_assign(seed) == coclust_assign(init = oracle's R4 sample): pins the GPU sampler."""
-    w = video_qkv(4, 8, 16, 2, 64, seed=3)
+@pytest.mark.parametrize("T,Hs,Ws,kq,kk", [(4, 8, 16, 12, 20), (1, 8, 8, 48, 60), (1, 10, 10, 100, 100),
+                                        (1, 30, 50, 700, 1024), (2, 16, 32, 1000, 1024)])
+def test_sampler_matches_oracle_via_explicit_init(pb, T, Hs, Ws, kq, kk):
+    """coclust_assign(seed) == coclust_assign(init = oracle's R4 sample): pins the GPU sampler,
+    including collision-heavy draws (K close to N: Floyd's j_i picks and draws t_i >= N - K)."""
+    w = video_qkv(T, Hs, Ws, 2, 64, seed=3)
     N = w.q.shape[2]
-    iq = np.stack([svoo.sample_anchor_indices(N, 12, 99, 0, h, 2, 0) for h in range(2)])[None]
-    ik = np.stack([svoo.sample_anchor_indices(N, 20, 99, 0, h, 2, 1) for h in range(2)])[None]
-    a = pb.coclust_assign(w.q.cuda(), w.k.cuda(), 12, 20, 1, seed=99)
-    b = pb.coclust_assign(w.q.cuda(), w.k.cuda(), 12, 20, 1, seed=12345,
+    iq = np.stack([svoo.sample_anchor_indices(N, kq, 99, 0, h, 2, 0) for h in range(2)])[None]
+    ik = np.stack([svoo.sample_anchor_indices(N, kk, 99, 0, h, 2, 1) for h in range(2)])[None]
+    a = pb.coclust_assign(w.q.cuda(), w.k.cuda(), kq, kk, 1, seed=99)
+    b = pb.coclust_assign(w.q.cuda(), w.k.cuda(), kq, kk, 1, seed=12345,
                           init_q=torch.from_numpy(iq.astype(np.int32)).cuda(),
                           init_k=torch.from_numpy(ik.astype(np.int32)).cuda())
     for key in a:
