@@ -392,21 +392,29 @@ def test_attn_singleton_keys_pick_value(pb):
 
 # ------------------------------------------------------------------------- P6 end to end
 def test_fused_toy_end_to_end(pb):
+    """P6 on the toy config: the first sampler seed whose oracle run has no near-tie in any
+    half-step (every gap >= 1e-4; seeds 3 and 14 of the first 60 qualify) must give identical
+    labels end to end and an output within P5.  Seeds with near-ties are covered by the chained
+    teacher-forced tests."""
     w = config_workload("toy")
-    budget = torch.tensor([0.3], dtype=torch.float32)
-    r = pb.coclust_assign(w.q.cuda(), w.k.cuda(), 16, 16, 3, seed=0)
-    O = pb.coclust_sparse_attention(w.q.cuda(), w.k.cuda(), w.v.cuda(), 16, 16, 3, budget.cuda(), seed=0)
-    torch.cuda.synchronize()
     Q, K, V = f64(w.q[0, 0]), f64(w.k[0, 0]), f64(w.v[0, 0])
-    ref = svoo.coclust_sparse_attention_head(Q, K, V, 16, 16, 3, 0, 0.3, 0.95, 0.1, svoo.RULE_DENSITY)
-    min_gap = min(float(np.min(t["gap"])) for t in ref.cc.trace)
-    if min_gap >= GAP_TOL:
-        assert np.array_equal(r["lq"][0, 0].cpu().numpy(), ref.cc.Lq)
-        assert np.array_equal(r["lk"][0, 0].cpu().numpy(), ref.cc.Lk)
-        err = np.abs(f64(O[0, 0]) - ref.O)
-        assert err.max() <= ATOL_MAX and err.mean() <= ATOL_MEAN
-    else:
-        pytest.skip(f"toy seed has a near-tie (min gap {min_gap:.2e}); teacher-forced tests cover it")
+    seed = ref = None
+    for s_ in range(60):
+        r_ = svoo.coclust_sparse_attention_head(Q, K, V, 16, 16, 3, s_, 0.3, 0.95, 0.1, svoo.RULE_DENSITY)
+        if min(float(np.min(t["gap"])) for t in r_.cc.trace) >= GAP_TOL:
+            seed, ref = s_, r_
+            break
+    assert seed is not None, "no near-tie-free toy seed in 0..59"
+    budget = torch.tensor([0.3], dtype=torch.float32)
+    r = pb.coclust_assign(w.q.cuda(), w.k.cuda(), 16, 16, 3, seed=seed)
+    O = pb.coclust_sparse_attention(w.q.cuda(), w.k.cuda(), w.v.cuda(), 16, 16, 3, budget.cuda(), seed=seed)
+    torch.cuda.synchronize()
+    assert np.array_equal(r["lq"][0, 0].cpu().numpy(), ref.cc.Lq)
+    assert np.array_equal(r["lk"][0, 0].cpu().numpy(), ref.cc.Lk)
+    assert np.array_equal(r["perm_q"][0, 0].cpu().numpy(), ref.perm_q)
+    assert np.array_equal(r["offs_k"][0, 0].cpu().numpy(), ref.offs_k)
+    err = np.abs(f64(O[0, 0]) - ref.O)
+    assert err.max() <= ATOL_MAX and err.mean() <= ATOL_MEAN
 
 
 @pytest.mark.parametrize("T,Hs,Ws,kq,kk", [(4, 8, 16, 12, 20), (1, 8, 8, 48, 60), (1, 10, 10, 100, 100),
