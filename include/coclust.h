@@ -168,7 +168,8 @@ cs_status block_select_ex(int B, int H, int kq, int kk, int d, const float* cq, 
                           int32_t* n_keep_rows, int32_t* kept, void* ws, size_t ws_bytes,
                           void* stream);
 
-/* Block-sparse attention over the kept blocks:
+/* Block-sparse attention over the kept blocks.  (Environment CS_ATTN_PERSIST=1 selects the
+ * bit-identical persistent variant of the kernel, one CTA per SM over the work items.)
  *   for query i in cluster a: o_i = sum_{j: L_k(j) in kept[a]} softmax_j(q_i.k_j * scale) v_j,
  * written in ORIGINAL token order (the inverse permutation is fused into the stores).  bf16 MMA,
  * fp32 accumulation and softmax, bf16 P (R15).  scale > 0 (1/sqrt(d) for the paper). */

@@ -4,6 +4,7 @@
 #include <cuda.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -286,12 +287,22 @@ cs_status run_attn(int B, int H, int N, int d, int kq, int kk, const int32_t* pe
     CS_CHECK(make_map_2d(&kv.v[i], sc.vp, (uint64_t)BH * N, d, 8u << i));
   }
   if (ev) CS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(ev[2]), st), "event");
-  CS_CUDA(launch_bsa_fwd(&tq, &kv, BH, H, N, d, kq, kk, perm_q, offs_q, offs_k, n_keep, n_rows, kept,
-                         sc.item_start, worklist_upper_bound(N, kq), scale,
-                         static_cast<__nv_bfloat16*>(o.ptr), o.sb, po ? po->s_head : o.sh,
-                         po ? po->s_tok : o.sn, po ? static_cast<const uint64_t*>(po->ptrs) : nullptr,
-                         po ? po->n_per_rank : 0, po ? po->head_base : 0, st),
-          "bsa_fwd");
+  // opt-in persistent attention kernel (attn_persist.cu; measured neutral on Wan14B / Wan1.3B)
+  const bool persist = getenv("CS_ATTN_PERSIST") != nullptr;
+  if (persist)
+    CS_CUDA(launch_bsa_fwd_persist(&tq, &kv, BH, H, N, d, kq, kk, perm_q, offs_q, offs_k, n_keep, n_rows, kept,
+                                   sc.item_start, worklist_upper_bound(N, kq), scale,
+                                   static_cast<__nv_bfloat16*>(o.ptr), o.sb, po ? po->s_head : o.sh,
+                                   po ? po->s_tok : o.sn, po ? static_cast<const uint64_t*>(po->ptrs) : nullptr,
+                                   po ? po->n_per_rank : 0, po ? po->head_base : 0, st),
+            "bsa_fwd_persist");
+  else
+    CS_CUDA(launch_bsa_fwd(&tq, &kv, BH, H, N, d, kq, kk, perm_q, offs_q, offs_k, n_keep, n_rows, kept,
+                           sc.item_start, worklist_upper_bound(N, kq), scale,
+                           static_cast<__nv_bfloat16*>(o.ptr), o.sb, po ? po->s_head : o.sh,
+                           po ? po->s_tok : o.sn, po ? static_cast<const uint64_t*>(po->ptrs) : nullptr,
+                           po ? po->n_per_rank : 0, po ? po->head_base : 0, st),
+            "bsa_fwd");
   if (ev) CS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(ev[3]), st), "event");
   return CS_OK;
 }
