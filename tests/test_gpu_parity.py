@@ -647,3 +647,22 @@ def test_persistent_attention_variant_matches(pb, monkeypatch):
     torch.cuda.synchronize()
     assert torch.equal(got, ref)
     assert torch.equal(got2, ref2)
+
+
+def test_attn_many_small_clusters_1024(pb):
+    """K_q = K_k = 1024 (the ABI maximum) on N = 8192: query clusters of ~8 rows (every item a
+    single-tile split-KV item), key clusters of ~8 keys (one 8-row unit each, heavy masking).
+    The whole layer against the oracle's masked attention on the GPU's partition."""
+    w = video_qkv(4, 32, 64, 1, 128, seed=80)
+    q, k, v = w.q.cuda(), w.k.cuda(), w.v.cuda()
+    budget = torch.tensor([0.15], dtype=torch.float32).cuda()
+    st = pb.coclust_assign(q, k, 1024, 1024, 2, seed=1)
+    n_keep, kept = pb.block_select(st["cq"], st["ck"], st["offs_q"], st["offs_k"], budget, 0.95, 0.1, pb.RULE_FIXED)
+    o = pb.coclust_sparse_attention(q, k, v, 1024, 1024, 2, budget, seed=1, rule=pb.RULE_FIXED)
+    torch.cuda.synchronize()
+    n = int(n_keep[0, 0])
+    assert n == 154
+    ref = svoo.sparse_attention(f64(w.q[0, 0]), f64(w.k[0, 0]), f64(w.v[0, 0]), st["lq"][0, 0].cpu().numpy(),
+                                st["lk"][0, 0].cpu().numpy(), kept[0, 0, :, :n].cpu().numpy())
+    err = np.abs(f64(o[0, 0]) - ref)
+    assert err.max() <= ATOL_MAX and err.mean() <= ATOL_MEAN, (err.max(), err.mean())
