@@ -116,3 +116,39 @@ def test_binding_refuses_cpu_tensors():
     x = torch.zeros(1, 1, 64, 64, dtype=torch.bfloat16)
     with pytest.raises(ValueError):
         pb.coclust_sparse_attention(x, x, x, 4, 4, 1, torch.ones(1))
+
+
+def test_extension_entry_argument_errors(L):
+    """Host-side validation of the NEXT-2/3/4 and multi-GPU entries (no launch, no GPU needed)."""
+    import paper_2603_18636_b200 as pb
+    q = _bf16()
+    # block_select_ex: unknown flag bits; per-row counts requested without their output
+    f = lambda flags, rows: L.block_select_ex(1, 2, 8, 16, 64, FAKE, FAKE, FAKE, FAKE, FAKE, 0.95, 0.1, 0, flags,
+                                              FAKE, rows, FAKE, FAKE, 1 << 30, None)
+    assert f(0x40, FAKE) == 3
+    assert f(pb.SEL_PER_ROW, None) == 1
+    # fused layer with unknown flags
+    o = pb._BF16Out(FAKE, 0, 0, 128)
+    st = L.coclust_sparse_attention_ex(1, 1, 256, 128, q, q, q, 16, 16, 2, 0, 0, 0, FAKE, 0.95, 0.1, 0, 0x8000,
+                                       0.1, o, FAKE, 1 << 40, None, None)
+    assert st == 3
+    # k-means half-step: too many centroids
+    assert L.kmeans_assign_step(1, 1, 256, 128, q, 2000, FAKE, FAKE, FAKE, 1 << 30, None) == 3
+    # profiler: tau, passes, NULL density
+    g = lambda tau=0.95, passes=0, dens=FAKE: L.attention_density(1, 1, 256, 128, q, q, tau, 0.1, passes, None,
+                                                                  dens, FAKE, 1 << 30, None)
+    assert g(tau=0.0) == 3 and g(passes=9) == 3 and g(dens=None) == 1
+    # peer barrier bounds
+    assert L.cs_peer_barrier(0, 0, FAKE, 1, None) == 3
+    assert L.cs_peer_barrier(2, 2, FAKE, 1, None) == 3
+    assert L.cs_peer_barrier(2, 1, FAKE, 0, None) == 3
+    assert L.cs_peer_barrier(2, 1, None, 1, None) == 1
+    # peer-output layer: P * n_per_rank must equal N
+    po = pb._PeerOut(FAKE, 2, 100, 0, 128 * 4, 128)
+    st = L.coclust_sparse_attention_peer(4, 256, 128, q, q, q, 16, 16, 2, 0, 0, 0, FAKE, 0.95, 0.1, 0, 0, 0.1,
+                                         ctypes.byref(po), FAKE, 1 << 40, None, None)
+    assert st == 2
+    # IPC helpers refuse NULL
+    assert L.cs_ipc_open(None, 0, ctypes.byref(ctypes.c_void_p())) == 1
+    assert L.cs_ipc_close(None, 0) == 1
+    assert L.cs_density_workspace_bytes(1, 2, 1000) > 0 and L.cs_density_workspace_bytes(0, 2, 1000) == 0
