@@ -528,3 +528,48 @@ def test_density_qk_and_schedule():
     assert np.allclose(sch["mu"], [[0.2, 0.6]]) and np.allclose(sch["sigma"], [[0.1, 0.1]])
     assert np.allclose(sch["d_hat"], [[0.2 + 0.1 * norm.ppf(0.95), min(1.0, 0.6 + 0.1 * norm.ppf(0.95))]])
     assert np.allclose(sch["s"], 1 - sch["d_hat"])
+
+
+def test_density_golden_spec_examples():
+    """SPEC:164-166 (P:1179-1185): uniform 10-wide rows at tau = 0.8 -> 0.8; one-hot rows -> 1/n;
+    row [0.5, 0.3, 0.1, 0.1] at tau = 0.8 -> 0.5."""
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))["recall_count"]
+    for ex in g:
+        p = np.asarray(ex["p"], np.float64)
+        d, c = svoo.attention_density(p[None], ex["tau"])
+        assert c[0] == ex["count"] and d == ex["count"] / len(p)
+    assert svoo.attention_density(np.eye(7), 0.3)[0] == 1 / 7
+
+
+def test_recall_counts_equal_row_density_of_softmaxed_abar():
+    """SURVEY 4.1 invariant: Recall's c_a (R9) is the attention-density prefix of the row
+    softmax(Abar_a / sqrt(d)) over the nonempty key blocks."""
+    Cq, Ck, sq, sk = _rand_select_inputs(11, kq=10, kk=40, d=16)
+    sel = svoo.select_blocks(Cq, Ck, sq, sk, 0.3, 0.9, 0.1, svoo.RULE_DENSITY, d_head=16)
+    ne = sk > 0
+    A = (Cq @ Ck.T)[:, ne] / 4.0
+    P = np.exp(A - A.max(1, keepdims=True))
+    P /= P.sum(1, keepdims=True)
+    _, c = svoo.attention_density(P, 0.9)
+    for a in range(len(sq)):
+        if sq[a] > 0:
+            assert sel.c[a] == c[a]
+
+
+def test_sparse_error_monotone_in_keep_ratio():
+    """SPEC invariant (nested masks): the median row error of the sparse output against
+    dense attention does not grow as rho grows (FIXED rule), and vanishes at rho = 1."""
+    rng = np.random.default_rng(12)
+    N, d = 256, 16
+    centers = rng.normal(size=(8, d)) * 2
+    lab = rng.integers(0, 8, N)
+    Q = centers[lab] + 0.7 * rng.normal(size=(N, d))
+    K = centers[lab] + 0.7 * rng.normal(size=(N, d))
+    V = rng.normal(size=(N, d))
+    dense = svoo.dense_attention(Q, K, V)
+    errs = []
+    for rho in (0.1, 0.25, 0.5, 0.75, 1.0):
+        r = svoo.coclust_sparse_attention_head(Q, K, V, 8, 16, 2, 0, rho, 0.95, 0.1, svoo.RULE_FIXED)
+        errs.append(float(np.median(np.linalg.norm(r.O - dense, axis=1))))
+    assert all(b <= a + 1e-12 for a, b in zip(errs, errs[1:])), errs
+    assert errs[-1] < 1e-12
