@@ -375,7 +375,10 @@ __global__ void __launch_bounds__(256) k_seg_mean(XView x, int N, int K, int nwc
                                                   __nv_bfloat16* __restrict__ xperm) {
   constexpr int LPR = D / 8;        // lanes per row: 16-byte (8 x bf16) vector per lane
   constexpr int RPW = 32 / LPR;     // rows per warp instruction (2 or 4)
-  constexpr int NW = 8, U = 8;      // warps, rows in flight per lane group
+#ifndef CS_SEG_U
+#define CS_SEG_U 8
+#endif
+  constexpr int NW = 8, U = CS_SEG_U;  // warps, rows in flight per lane group
   __shared__ float part[NW * RPW][D];
   const int bh = blockIdx.y;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
