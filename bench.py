@@ -321,7 +321,8 @@ def run_ours(args):
         torch.cuda.current_stream().wait_stream(cs)
         torch.cuda.synchronize()
         graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph):
+        # thread_local: the NCCL watchdog thread may query events while this thread captures
+        with torch.cuda.graph(graph, capture_error_mode="thread_local"):
             step()
         for _ in range(max(args.warmup, 1)):
             graph.replay()

@@ -156,7 +156,7 @@ def run_heads(a):
             if a.graph:
                 torch.cuda.synchronize()
                 g = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(g):
+                with torch.cuda.graph(g, capture_error_mode="thread_local"):
                     call()
                 call = g.replay
                 call()
