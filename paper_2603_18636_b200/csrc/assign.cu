@@ -18,6 +18,10 @@
 #include "kernels.cuh"
 
 namespace cs {
+#ifndef CS_ASSIGN_GROUPMAX
+#define CS_ASSIGN_GROUPMAX 1
+#endif
+
 namespace asg {
 
 constexpr int BM = 128, TILES = 2, NSTW = 4, NTHREADS = 320, NCH_MAX = 128;
@@ -153,6 +157,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const int bh = u / units_per_head, n0 = (u % units_per_head) * (TILES * BM);
       float best = -INFINITY;
       int best_j = 0;
+#if CS_ASSIGN_GROUPMAX
+      // grouped argmax: per 16 columns a 3-input max tree (8 FMNMX) and one compare; the group
+      // that raised the running max is kept in registers and searched once per row at the end.
+      // Same result as the serial scan: exact fp32 compares, ties -> lowest index (strict > across
+      // groups, first equal element inside the winning group).
+      float keep[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) keep[i] = -INFINITY;
+#endif
       for (int c = 0; c < nchunks; ++c, ++gc) {
         const int buf = gc & 1;
         mbar_wait(acc_full + buf, (gc >> 1) & 1);
@@ -172,6 +185,27 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             }
           }
           tmem_wait_ld();
+#if CS_ASSIGN_GROUPMAX
+          float xs[16];
+          const int jg = jbase + c0;
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            xs[i] = __uint_as_float(v[i]);
+            if constexpr (BIAS) xs[i] += bs[i];
+          }
+          if (jg + 16 > ks) {  // ragged last group (warp-uniform branch)
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              if (jg + i >= ks) xs[i] = -INFINITY;
+          }
+          const float m = fmaxf(fmax3(fmax3(xs[0], xs[1], xs[2]), fmax3(xs[3], xs[4], xs[5]), fmax3(xs[6], xs[7], xs[8])),
+                                fmax3(fmax3(xs[9], xs[10], xs[11]), fmax3(xs[12], xs[13], xs[14]), xs[15]));
+          const bool up = m > best;
+          best = up ? m : best;
+          best_j = up ? jg : best_j;
+#pragma unroll
+          for (int i = 0; i < 16; ++i) keep[i] = up ? xs[i] : keep[i];
+#else
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             const int j = jbase + c0 + i;
@@ -179,10 +213,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             if constexpr (BIAS) x += bs[i];
             if (j < ks && x > best) { best = x; best_j = j; }
           }
+#endif
         }
         tc_fence_before();
         mbar_arrive(acc_empty + buf);
       }
+#if CS_ASSIGN_GROUPMAX
+      {
+        int off = 15;
+#pragma unroll
+        for (int i = 15; i >= 0; --i) off = keep[i] == best ? i : off;
+        best_j += off;
+      }
+#endif
       const int n = n0 + t * BM + r;
       if (n < N) labels[(size_t)bh * N + n] = best_j;
     }
