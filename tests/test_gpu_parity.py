@@ -100,6 +100,33 @@ def test_assign_step(pb, d, N, ka, ks):
         _check_labels(lab[0, h].cpu().numpy(), res, f"h={h}")
 
 
+@pytest.mark.parametrize("kmeans", [False, True])
+def test_assign_exact_ties_pick_lowest_index(pb, kmeans):
+    """R2 on exact ties: duplicated centroid rows give bit-identical scores, so the argmax epilogue
+    must return the lower index — pairs inside one 16-column group, across groups, across 128-column
+    chunks and in the ragged last group.  Labels must equal the oracle run on the de-duplicated
+    centroid set (mapped back to the lower index) outside its near-tie band."""
+    d, N, ka, ks = 128, 4096, 100, 500
+    dups = {6: 5, 17: 3, 300: 10, 499: 130}  # higher duplicate -> lower original
+    w = video_qkv(4, 16, N // 64, 1, d, seed=77)
+    N = w.k.shape[2]
+    g = torch.Generator().manual_seed(5)
+    ca = torch.randn(1, 1, ka, d, generator=g)
+    cs = torch.randn(1, 1, ks, d, generator=g)
+    for hi, lo in dups.items():
+        cs[0, 0, hi] = cs[0, 0, lo]
+    if kmeans:
+        lab = pb.kmeans_assign_step(w.k.cuda(), cs.cuda())[0, 0].cpu().numpy()
+    else:
+        lab = pb.coclust_assign_step(w.k.cuda(), ca.cuda(), cs.cuda())[0, 0].cpu().numpy()
+    assert not np.isin(lab, list(dups)).any()
+    keep = np.array([j for j in range(ks) if j not in dups])
+    X, C = f64(w.k[0, 0]), cs[0, 0].double().numpy()[keep]
+    res = svoo.kmeans_step(X, C) if kmeans else svoo.assign_step(X, ca[0, 0].double().numpy(), C)
+    ref, clear = res.labels, res.gap >= GAP_TOL
+    assert np.array_equal(lab[clear], keep[ref][clear])
+
+
 def test_assign_identity_anchor_is_cosine(pb):
     """ka = d and C_anchor = I: the half-step is cosine nearest-centroid (a textbook rule)."""
     d, N, ks = 64, 3000, 40
