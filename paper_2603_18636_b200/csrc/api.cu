@@ -231,7 +231,7 @@ cs_status run_assign_step(int B, int H, int N, int d, cs_bf16_in x, int ka, cons
   CS_CUDA(launch_anchor_prep(ca, ka, cself, ks, ks_pad, BH, d, sc.gamma, sc.wsplit, st), "anchor_prep");
   CUtensorMap tx, tw;
   CS_CHECK(make_map_x(&tx, x, B, H, N, d));
-  CS_CHECK(make_map_2d(&tw, sc.wsplit, (uint64_t)BH * ks_pad, 2 * d, nch));
+  CS_CHECK(make_map_2d(&tw, sc.wsplit, (uint64_t)BH * ks_pad, 2 * d, assign_box_rows(ks)));
   CS_CUDA(launch_assign_gemm(&tx, &tw, B, H, N, d, ks, nch, ks_pad, nullptr, labels, st), "assign_gemm");
   return CS_OK;
 }
@@ -244,7 +244,7 @@ cs_status run_kmeans_step(int B, int H, int N, int d, cs_bf16_in x, int ks, cons
   CS_CUDA(launch_kmeans_prep(cself, ks, ks_pad, BH, d, sc.wsplit, sc.bias, st), "kmeans_prep");
   CUtensorMap tx, tw;
   CS_CHECK(make_map_x(&tx, x, B, H, N, d));
-  CS_CHECK(make_map_2d(&tw, sc.wsplit, (uint64_t)BH * ks_pad, 2 * d, nch));
+  CS_CHECK(make_map_2d(&tw, sc.wsplit, (uint64_t)BH * ks_pad, 2 * d, assign_box_rows(ks)));
   CS_CUDA(launch_assign_gemm(&tx, &tw, B, H, N, d, ks, nch, ks_pad, sc.bias, labels, st), "assign_gemm");
   return CS_OK;
 }

@@ -240,7 +240,223 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
 }  // namespace asg
 
-int assign_chunk_n(int ks) { return ks <= asg::NCH_MAX ? (ks + 15) / 16 * 16 : asg::NCH_MAX; }
+// ---------------------------------------------------------------------------------------------
+// CTA-pair variant (cta_group::2) for centroid sides of more than one chunk (the key side, K_k >
+// 128).  A cluster of 2 CTAs (one per SM of a TPC) owns a unit of 256 tokens: CTA r holds token
+// tile r (rows n0 + 128 r ...), and each 64-column W slab of an N <= 256 chunk is split by rows
+// between the two CTAs (CTA r loads chunk rows [r nch/2, (r+1) nch/2)).  The leader issues M=256
+// MMAs; each CTA's TMEM receives its own 128 token rows x nch columns.  Per SM this reads 4 KB of
+// A and nch/2 x 32 B of B per K=16 step and receives half of the streamed W (shared-
+// memory budget), and when the head's whole W fits the 8-slab ring (nchunks x slabs = 8, e.g.
+// K_k = 500 -> 2 chunks of 256) it stays resident across the head's units, so W is not re-streamed.
+// Warps 0-3: epilogue (thread = token row), warp 4: TMA producer, warp 5: TMEM allocator + MMA
+// issuer (leader only).
+namespace asg2 {
+constexpr int BM = 128, NSTW = 8, NTHREADS = 192, NCH_MAX = 256;
+constexpr int WARP_PRODUCER = 4, WARP_MMA = 5;
+
+template <int D>
+struct Smem {
+  static constexpr int HALVES = D / 64;
+  static constexpr int XT = BM * D * 2;             // this CTA's 128-token tile
+  static constexpr int HALF_X = BM * 128;
+  static constexpr int SLAB = (NCH_MAX / 2) * 128;  // this CTA's half of a 64-column W slab
+  static constexpr int OFF_X = 0;
+  static constexpr int OFF_W = OFF_X + 2 * XT;
+  static constexpr int OFF_BAR = OFF_W + NSTW * SLAB;
+  // x_full[2], x_empty[2], w_full[8], w_empty[8], acc_full[2], acc_empty[2]
+  static constexpr int OFF_MISC = OFF_BAR + 24 * 8;
+  static constexpr int BYTES = OFF_MISC + 16;
+  static constexpr int ALLOC = BYTES + 1024;
+};
+
+template <int D, bool BIAS>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
+    k_assign_pair(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_w,
+                  int H, int N, int ks, int nch, int ks_pad, int units_per_head, int num_units,
+                  const float* __restrict__ bias, int32_t* __restrict__ labels) {
+  using L = Smem<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::OFF_BAR);
+  uint64_t* x_full = bars;
+  uint64_t* x_empty = bars + 2;
+  uint64_t* w_full = bars + 4;
+  uint64_t* w_empty = bars + 4 + NSTW;
+  uint64_t* acc_full = bars + 4 + 2 * NSTW;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + L::OFF_MISC);
+
+  const int warp = warp_id(), lane = lane_id();
+  const uint32_t rank = cluster_ctarank();
+  const int nchunks = ks_pad / nch;
+  const int half = nch / 2;
+  const int ncl = gridDim.x / 2, cid = blockIdx.x / 2;
+  const int upc = (num_units + ncl - 1) / ncl;
+  const int u_begin = cid * upc, u_end = min(num_units, u_begin + upc);
+  constexpr int SLABS = 2 * D / 64;
+  const bool can_reside = nchunks * SLABS == NSTW;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < 2; ++s) { mbar_init(x_full + s, 1); mbar_init(x_empty + s, 1); }
+    for (int s = 0; s < NSTW; ++s) { mbar_init(w_full + s, 1); mbar_init(w_empty + s, 1); }
+    for (int t = 0; t < 2; ++t) { mbar_init(acc_full + t, 1); mbar_init(acc_empty + t, 8); }
+    fence_barrier_init();
+  }
+  if (warp == WARP_MMA) tmem_alloc_pair(tmem_slot, 512);
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == WARP_PRODUCER) {
+    if (lane == 0) {
+      tma_prefetch_desc(&tm_x);
+      tma_prefetch_desc(&tm_w);
+      int g = 0, it = 0, prev_bh = -1;
+      for (int u = u_begin; u < u_end; ++u, ++it) {
+        const int bh = u / units_per_head, n0 = (u % units_per_head) * (2 * BM);
+        const int b = bh / H, h = bh % H;
+        const int xs = it & 1;
+        mbar_wait(x_empty + xs, ((it >> 1) & 1) ^ 1);
+        const uint32_t xf = mapa_shared(smem_u32(x_full + xs), 0);
+        if (rank == 0) mbar_arrive_expect_tx(x_full + xs, 2 * L::XT);
+        for (int hf = 0; hf < L::HALVES; ++hf)
+          tma_load_4d_pair(sm + L::OFF_X + xs * L::XT + hf * L::HALF_X, &tm_x, hf * 64, n0 + (int)rank * BM, h, b,
+                           xf);
+        const bool resident = can_reside && bh == prev_bh;
+        for (int c = 0; c < nchunks; ++c)
+          for (int s = 0; s < SLABS; ++s, ++g) {
+            const int stage = g % NSTW;
+            mbar_wait(w_empty + stage, ((g / NSTW) & 1) ^ 1);
+            if (resident) {
+              if (rank == 0) mbar_arrive(w_full + stage);
+            } else {
+              if (rank == 0) mbar_arrive_expect_tx(w_full + stage, nch * 128);
+              tma_load_2d_pair(sm + L::OFF_W + stage * L::SLAB, &tm_w, s * 64, bh * ks_pad + c * nch + (int)rank * half,
+                               mapa_shared(smem_u32(w_full + stage), 0));
+            }
+          }
+        prev_bh = bh;
+      }
+    }
+  } else if (warp == WARP_MMA) {
+    if (lane == 0 && rank == 0) {
+      const uint32_t idesc = idesc_bf16(2 * BM, nch, 0, 0);
+      const uint32_t sX = smem_u32(sm + L::OFF_X), sW = smem_u32(sm + L::OFF_W);
+      int g = 0, gc = 0, it = 0;
+      for (int u = u_begin; u < u_end; ++u, ++it) {
+        const int xs = it & 1;
+        mbar_wait(x_full + xs, (it >> 1) & 1);
+        for (int c = 0; c < nchunks; ++c, ++gc) {
+          const int buf = gc & 1;
+          mbar_wait(acc_empty + buf, ((gc >> 1) & 1) ^ 1);
+          tc_fence_after();
+          for (int s = 0; s < SLABS; ++s, ++g) {
+            const int stage = g % NSTW;
+            mbar_wait(w_full + stage, (g / NSTW) & 1);
+            tc_fence_after();
+            const int xh = s % L::HALVES;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const uint64_t ad = smem_desc_sw128(sX + xs * L::XT + xh * L::HALF_X + k * 32, 16, 1024);
+              const uint64_t bd = smem_desc_sw128(sW + stage * L::SLAB + k * 32, 16, 1024);
+              mma_ss_pair(tmem + buf * NCH_MAX, ad, bd, idesc, (s > 0 || k > 0) ? 1u : 0u);
+            }
+            mma_commit_pair(w_empty + stage);
+          }
+          mma_commit_pair(acc_full + buf);
+        }
+        mma_commit_pair(x_empty + xs);
+      }
+    }
+    __syncwarp();
+  } else {
+    // epilogue: grouped running argmax (as k_assign), ties -> lowest index
+    const int r = warp * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+    int gc = 0;
+    for (int u = u_begin; u < u_end; ++u) {
+      const int bh = u / units_per_head, n0 = (u % units_per_head) * (2 * BM);
+      float best = -INFINITY;
+      int best_j = 0;
+      float keep[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) keep[i] = -INFINITY;
+      for (int c = 0; c < nchunks; ++c, ++gc) {
+        const int buf = gc & 1;
+        mbar_wait(acc_full + buf, (gc >> 1) & 1);
+        tc_fence_after();
+        const uint32_t t_acc = tmem + lane_off + buf * NCH_MAX;
+        const int jbase = c * nch;
+        for (int c0 = 0; c0 < nch; c0 += 16) {
+          uint32_t v[16];
+          tmem_ld16(t_acc + c0, v);
+          float bs[16];
+          if constexpr (BIAS) {
+            const float4* b4 = reinterpret_cast<const float4*>(bias + (size_t)bh * ks_pad + jbase + c0);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float4 q = __ldg(b4 + i);
+              bs[4 * i] = q.x; bs[4 * i + 1] = q.y; bs[4 * i + 2] = q.z; bs[4 * i + 3] = q.w;
+            }
+          }
+          tmem_wait_ld();
+          float xs[16];
+          const int jg = jbase + c0;
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            xs[i] = __uint_as_float(v[i]);
+            if constexpr (BIAS) xs[i] += bs[i];
+          }
+          if (jg + 16 > ks) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              if (jg + i >= ks) xs[i] = -INFINITY;
+          }
+          const float m = fmaxf(fmax3(fmax3(xs[0], xs[1], xs[2]), fmax3(xs[3], xs[4], xs[5]), fmax3(xs[6], xs[7], xs[8])),
+                                fmax3(fmax3(xs[9], xs[10], xs[11]), fmax3(xs[12], xs[13], xs[14]), xs[15]));
+          const bool up = m > best;
+          best = up ? m : best;
+          best_j = up ? jg : best_j;
+#pragma unroll
+          for (int i = 0; i < 16; ++i) keep[i] = up ? xs[i] : keep[i];
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(acc_empty + buf), 0));
+      }
+      int off = 15;
+#pragma unroll
+      for (int i = 15; i >= 0; --i) off = keep[i] == best ? i : off;
+      best_j += off;
+      const int n = n0 + (int)rank * BM + r;
+      if (n < N) labels[(size_t)bh * N + n] = best_j;
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == WARP_MMA) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem, 512);
+  }
+}
+}  // namespace asg2
+
+#ifndef CS_ASSIGN_PAIR
+#define CS_ASSIGN_PAIR 1
+#endif
+// one chunk (ks <= 128): single-CTA kernel, N = ks rounded to 16, W resident across a head's units;
+// more: the CTA-pair kernel with ceil(ks / 256) chunks of N <= 256 (a multiple of 32, so each CTA
+// holds a multiple of 16 rows)
+static bool use_pair(int ks) { return CS_ASSIGN_PAIR && ks > asg::NCH_MAX; }
+int assign_chunk_n(int ks) {
+  if (ks <= asg::NCH_MAX) return (ks + 15) / 16 * 16;
+  if (!use_pair(ks)) return asg::NCH_MAX;
+  const int nchunks = (ks + asg2::NCH_MAX - 1) / asg2::NCH_MAX;
+  return ((ks + nchunks - 1) / nchunks + 31) / 32 * 32;
+}
+int assign_box_rows(int ks) { return use_pair(ks) ? assign_chunk_n(ks) / 2 : assign_chunk_n(ks); }
 
 cudaError_t launch_assign_gemm(const CUtensorMap* tm_x, const CUtensorMap* tm_w, int B, int H, int N,
                                int d, int ks, int nch, int ks_pad, const float* bias, int32_t* labels,
@@ -254,6 +470,25 @@ cudaError_t launch_assign_gemm(const CUtensorMap* tm_x, const CUtensorMap* tm_w,
   }
   const int units_per_head = (N + asg::TILES * asg::BM - 1) / (asg::TILES * asg::BM);
   const int num_units = units_per_head * B * H;
+  if (use_pair(ks)) {
+    const int pairs = num_units < num_sms / 2 ? num_units : num_sms / 2;
+    auto launch2 = [&](auto kfn, int smem) -> cudaError_t {
+      cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e != cudaSuccess) return e;
+      kfn<<<2 * pairs, asg2::NTHREADS, smem, st>>>(*tm_x, *tm_w, H, N, ks, nch, ks_pad, units_per_head, num_units,
+                                                    bias, labels);
+      return cudaSuccess;
+    };
+    cudaError_t e;
+    if (d == 128)
+      e = bias ? launch2(asg2::k_assign_pair<128, true>, asg2::Smem<128>::ALLOC)
+               : launch2(asg2::k_assign_pair<128, false>, asg2::Smem<128>::ALLOC);
+    else
+      e = bias ? launch2(asg2::k_assign_pair<64, true>, asg2::Smem<64>::ALLOC)
+               : launch2(asg2::k_assign_pair<64, false>, asg2::Smem<64>::ALLOC);
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+  }
   const int grid = num_units < num_sms ? num_units : num_sms;
   auto launch = [&](auto kfn, int smem) -> cudaError_t {
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

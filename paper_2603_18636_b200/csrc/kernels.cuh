@@ -46,6 +46,7 @@ cudaError_t launch_permute_rows(XView x, int BH, int N, int d, const int32_t* pe
 // tm_x: 4D map over x {d, N, H, B} box {64, 128, 1, 1}; tm_w: 2D map over Wsplit {2d, BH*ks_pad}
 // box {64, nch}.
 int assign_chunk_n(int ks);  // centroid columns per TMEM chunk (UMMA N)
+int assign_box_rows(int ks);  // W rows per TMA box (half a chunk for the CTA-pair kernel)
 cudaError_t launch_assign_gemm(const CUtensorMap* tm_x, const CUtensorMap* tm_w, int B, int H, int N,
                                int d, int ks, int nch, int ks_pad, const float* bias, int32_t* labels,
                                cudaStream_t st);
