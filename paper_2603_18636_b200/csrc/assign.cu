@@ -252,38 +252,40 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 // Warps 0-3: epilogue (thread = token row), warp 4: TMA producer, warp 5: TMEM allocator + MMA
 // issuer (leader only).
 namespace asg2 {
-constexpr int BM = 128, NSTW = 8, NTHREADS = 192, NCH_MAX = 256;
+constexpr int BM = 128, NTHREADS = 192, NCH_MAX = 256;
 constexpr int WARP_PRODUCER = 4, WARP_MMA = 5;
 
-template <int D>
+// XST token-tile stages, NSTW W-slab stages; launched as (2, 8): the whole W of a head fits the
+// ring at K_k <= 512 (2 chunks x 4 slabs at d = 128)
+template <int D, int XST, int NSTW>
 struct Smem {
   static constexpr int HALVES = D / 64;
   static constexpr int XT = BM * D * 2;             // this CTA's 128-token tile
   static constexpr int HALF_X = BM * 128;
   static constexpr int SLAB = (NCH_MAX / 2) * 128;  // this CTA's half of a 64-column W slab
   static constexpr int OFF_X = 0;
-  static constexpr int OFF_W = OFF_X + 2 * XT;
+  static constexpr int OFF_W = OFF_X + XST * XT;
   static constexpr int OFF_BAR = OFF_W + NSTW * SLAB;
-  // x_full[2], x_empty[2], w_full[8], w_empty[8], acc_full[2], acc_empty[2]
-  static constexpr int OFF_MISC = OFF_BAR + 24 * 8;
+  // x_full[XST], x_empty[XST], w_full[NSTW], w_empty[NSTW], acc_full[2], acc_empty[2]
+  static constexpr int OFF_MISC = OFF_BAR + (2 * XST + 2 * NSTW + 4) * 8;
   static constexpr int BYTES = OFF_MISC + 16;
   static constexpr int ALLOC = BYTES + 1024;
 };
 
-template <int D, bool BIAS>
+template <int D, bool BIAS, int XST, int NSTW>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     k_assign_pair(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_w,
                   int H, int N, int ks, int nch, int ks_pad, int units_per_head, int num_units,
                   const float* __restrict__ bias, int32_t* __restrict__ labels) {
-  using L = Smem<D>;
+  using L = Smem<D, XST, NSTW>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::OFF_BAR);
   uint64_t* x_full = bars;
-  uint64_t* x_empty = bars + 2;
-  uint64_t* w_full = bars + 4;
-  uint64_t* w_empty = bars + 4 + NSTW;
-  uint64_t* acc_full = bars + 4 + 2 * NSTW;
+  uint64_t* x_empty = bars + XST;
+  uint64_t* w_full = bars + 2 * XST;
+  uint64_t* w_empty = w_full + NSTW;
+  uint64_t* acc_full = w_empty + NSTW;
   uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + L::OFF_MISC);
 
@@ -298,7 +300,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   const bool can_reside = nchunks * SLABS == NSTW;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < 2; ++s) { mbar_init(x_full + s, 1); mbar_init(x_empty + s, 1); }
+    for (int s = 0; s < XST; ++s) { mbar_init(x_full + s, 1); mbar_init(x_empty + s, 1); }
     for (int s = 0; s < NSTW; ++s) { mbar_init(w_full + s, 1); mbar_init(w_empty + s, 1); }
     for (int t = 0; t < 2; ++t) { mbar_init(acc_full + t, 1); mbar_init(acc_empty + t, 8); }
     fence_barrier_init();
@@ -317,8 +319,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
       for (int u = u_begin; u < u_end; ++u, ++it) {
         const int bh = u / units_per_head, n0 = (u % units_per_head) * (2 * BM);
         const int b = bh / H, h = bh % H;
-        const int xs = it & 1;
-        mbar_wait(x_empty + xs, ((it >> 1) & 1) ^ 1);
+        const int xs = it % XST;
+        mbar_wait(x_empty + xs, ((it / XST) & 1) ^ 1);
         const uint32_t xf = mapa_shared(smem_u32(x_full + xs), 0);
         if (rank == 0) mbar_arrive_expect_tx(x_full + xs, 2 * L::XT);
         for (int hf = 0; hf < L::HALVES; ++hf)
@@ -346,8 +348,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
       const uint32_t sX = smem_u32(sm + L::OFF_X), sW = smem_u32(sm + L::OFF_W);
       int g = 0, gc = 0, it = 0;
       for (int u = u_begin; u < u_end; ++u, ++it) {
-        const int xs = it & 1;
-        mbar_wait(x_full + xs, (it >> 1) & 1);
+        const int xs = it % XST;
+        mbar_wait(x_full + xs, (it / XST) & 1);
         for (int c = 0; c < nchunks; ++c, ++gc) {
           const int buf = gc & 1;
           mbar_wait(acc_empty + buf, ((gc >> 1) & 1) ^ 1);
@@ -446,13 +448,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
 #ifndef CS_ASSIGN_PAIR
 #define CS_ASSIGN_PAIR 1
 #endif
-// one chunk (ks <= 128): single-CTA kernel, N = ks rounded to 16, W resident across a head's units;
-// more: the CTA-pair kernel with ceil(ks / 256) chunks of N <= 256 (a multiple of 32, so each CTA
-// holds a multiple of 16 rows)
+// ks <= 128 (one chunk, e.g. the query side): single-CTA kernel, N = ks rounded to 16, W resident
+// across a head's units (the pair kernel with 4 token stages measured slower there: 233 vs 186 us
+// at K_q = 100, an HBM-bound launch).  More: the CTA-pair kernel with ceil(ks / 256) chunks of
+// N <= 256 (a multiple of 32, so each CTA holds a multiple of 16 rows).  CS_ASSIGN_PAIR=0 builds
+// the single-CTA kernel for every side (A/B comparisons).
 static bool use_pair(int ks) { return CS_ASSIGN_PAIR && ks > asg::NCH_MAX; }
 int assign_chunk_n(int ks) {
-  if (ks <= asg::NCH_MAX) return (ks + 15) / 16 * 16;
-  if (!use_pair(ks)) return asg::NCH_MAX;
+  if (!use_pair(ks)) return ks <= asg::NCH_MAX ? (ks + 15) / 16 * 16 : asg::NCH_MAX;
   const int nchunks = (ks + asg2::NCH_MAX - 1) / asg2::NCH_MAX;
   return ((ks + nchunks - 1) / nchunks + 31) / 32 * 32;
 }
@@ -480,12 +483,13 @@ cudaError_t launch_assign_gemm(const CUtensorMap* tm_x, const CUtensorMap* tm_w,
       return cudaSuccess;
     };
     cudaError_t e;
+    using namespace asg2;
     if (d == 128)
-      e = bias ? launch2(asg2::k_assign_pair<128, true>, asg2::Smem<128>::ALLOC)
-               : launch2(asg2::k_assign_pair<128, false>, asg2::Smem<128>::ALLOC);
+      e = bias ? launch2(k_assign_pair<128, true, 2, 8>, Smem<128, 2, 8>::ALLOC)
+               : launch2(k_assign_pair<128, false, 2, 8>, Smem<128, 2, 8>::ALLOC);
     else
-      e = bias ? launch2(asg2::k_assign_pair<64, true>, asg2::Smem<64>::ALLOC)
-               : launch2(asg2::k_assign_pair<64, false>, asg2::Smem<64>::ALLOC);
+      e = bias ? launch2(k_assign_pair<64, true, 2, 8>, Smem<64, 2, 8>::ALLOC)
+               : launch2(k_assign_pair<64, false, 2, 8>, Smem<64, 2, 8>::ALLOC);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
   }
