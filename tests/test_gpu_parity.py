@@ -57,7 +57,7 @@ def test_permute_sorted_labels_and_single_token():
 
 
 # ------------------------------------------------------------------------- P2 centroid update
-@pytest.mark.parametrize("d,N,K", [(64, 2048, 16), (128, 8192, 100)])
+@pytest.mark.parametrize("d,N,K", [(64, 2048, 16), (128, 8192, 100), (128, 20000, 8), (64, 9000, 3)])
 def test_update_centroids(pb, d, N, K):
     w = random_qkv(1, 2, N, d, seed=3)
     lab = random_labels(2, N, K, seed=5, empty=(1,))
