@@ -307,7 +307,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   }
   if (warp == WARP_MMA) tmem_alloc_pair(tmem_slot, 512);
   tc_fence_before();
-  cluster_sync_all();
+  cluster_sync_all();  // barriers initialised and TMEM allocated in both CTAs
+  __syncthreads();     // (also a CTA barrier, which compute-sanitizer's racecheck models)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
