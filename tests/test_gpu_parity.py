@@ -86,7 +86,11 @@ def _check_labels(got, res, ctx=""):
 
 @pytest.mark.parametrize("d,N,ka,ks", [(64, 2048, 16, 16), (128, 8192, 100, 500),
                                        (128, 8192, 500, 100), (128, 3000, 37, 300), (64, 1000, 1, 7),
-                                       (128, 4096, 256, 1024)])
+                                       (128, 4096, 256, 1024),
+                                       # CTA-pair kernel shapes: d = 64, one chunk of 160 / 288 columns,
+                                       # 2 chunks at N % 256 != 0, 4 chunks of 224
+                                       (64, 4096, 50, 500), (64, 2000, 10, 129), (128, 2500, 20, 257),
+                                       (128, 1300, 30, 777)])
 def test_assign_step(pb, d, N, ka, ks):
     w = video_qkv(4, 16, max(1, N // 64), 2, d, seed=ka + ks)
     N = w.q.shape[2]
@@ -523,6 +527,7 @@ def test_clustering_reuse_cached_entry(pb):
 
 # ------------------------------------------------------------------------- NEXT-2 k-means baseline
 @pytest.mark.parametrize("d,N,ks", [(64, 2048, 16), (128, 8192, 500), (128, 3000, 100), (128, 4096, 1024),
+                                    (64, 3000, 300),
                                     (64, 1000, 1)])
 def test_kmeans_assign_step(pb, d, N, ks):
     """k-means half-step through the assignment GEMM with the -||c||^2/2 bias epilogue: labels
