@@ -542,19 +542,33 @@ __global__ void __launch_bounds__(256) k_csort_scatter(const int32_t* __restrict
 // ---------------------------------------------------------------------------------------------
 // x_perm[bh][p][:] = x[b,h,perm[bh][p],:].  grid (ceil(N/16), BH), block 256 (16 rows / block)
 // ---------------------------------------------------------------------------------------------
+#ifndef CS_PERM_U
+#define CS_PERM_U 4
+#endif
+constexpr int kPermU = CS_PERM_U;  // rows per thread: kPermU 16-byte loads in flight
 __global__ void __launch_bounds__(256) k_permute_rows(XView x, int N, int d,
                                                       const int32_t* __restrict__ perm,
                                                       __nv_bfloat16* __restrict__ xp) {
   const int bh = blockIdx.y;
   const int lanes_per_row = d / 8;  // 16-byte chunks per row
-  const int rows_per_block = 256 / lanes_per_row;
+  const int rows_per_pass = 256 / lanes_per_row;
   const int r = threadIdx.x / lanes_per_row, c = threadIdx.x % lanes_per_row;
-  const int p = blockIdx.x * rows_per_block + r;
-  if (p >= N) return;
-  const int tok = perm[(size_t)bh * N + p];
+  const int p0 = blockIdx.x * rows_per_pass * kPermU + r;
   const int b = bh / x.H, h = bh % x.H;
-  const uint4 v = *reinterpret_cast<const uint4*>(x.row(b, h, tok) + c * 8);
-  *reinterpret_cast<uint4*>(xp + ((size_t)bh * N + p) * d + c * 8) = v;
+  int tok[kPermU];
+  uint4 v[kPermU];
+#pragma unroll
+  for (int u = 0; u < kPermU; ++u) {
+    const int p = p0 + u * rows_per_pass;
+    tok[u] = p < N ? perm[(size_t)bh * N + p] : -1;
+  }
+#pragma unroll
+  for (int u = 0; u < kPermU; ++u)
+    if (tok[u] >= 0) v[u] = *reinterpret_cast<const uint4*>(x.row(b, h, tok[u]) + c * 8);
+#pragma unroll
+  for (int u = 0; u < kPermU; ++u)
+    if (tok[u] >= 0)
+      *reinterpret_cast<uint4*>(xp + ((size_t)bh * N + p0 + u * rows_per_pass) * d + c * 8) = v[u];
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -622,7 +636,7 @@ cudaError_t launch_csort(const int32_t* lab, int BH, int N, int K, int32_t* perm
 
 cudaError_t launch_permute_rows(XView x, int BH, int N, int d, const int32_t* perm,
                                 __nv_bfloat16* xp, cudaStream_t st) {
-  const int rows_per_block = 256 / (d / 8);
+  const int rows_per_block = 256 / (d / 8) * kPermU;
   k_permute_rows<<<dim3((N + rows_per_block - 1) / rows_per_block, BH), 256, 0, st>>>(x, N, d, perm, xp);
   return cudaGetLastError();
 }
