@@ -439,7 +439,16 @@ __global__ void __launch_bounds__(256) k_csort_hist(const int32_t* __restrict__ 
   __syncthreads();
   const int i0 = t * kSortTile, i1 = min(N, i0 + kSortTile);
   const int32_t* L = lab + (size_t)bh * N;
-  for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) atomicAdd(&sh_hist[L[i]], 1);
+  constexpr int RT = kSortTile / 256;  // labels per thread, all loads in flight before the atomics
+  int lbl[RT];
+#pragma unroll
+  for (int r = 0; r < RT; ++r) {
+    const int i = i0 + r * 256 + threadIdx.x;
+    lbl[r] = i < i1 ? L[i] : -1;
+  }
+#pragma unroll
+  for (int r = 0; r < RT; ++r)
+    if (lbl[r] >= 0) atomicAdd(&sh_hist[lbl[r]], 1);
   __syncthreads();
   int32_t* H = hist + ((size_t)bh * ntiles + t) * K;
   for (int c = threadIdx.x; c < K; c += blockDim.x) H[c] = sh_hist[c];
@@ -503,12 +512,20 @@ __global__ void __launch_bounds__(256) k_csort_scatter(const int32_t* __restrict
   const int i0 = t * kSortTile + w * (kSortTile / 8), i1 = min(N, i0 + kSortTile / 8);
   const unsigned lt = (1u << lane) - 1u;
   int* cw = wc + w * K;
-  for (int i = i0; i < i1; i += 32) {  // per-warp label counts
-    const int me = i + lane;
-    const bool valid = me < i1;
-    const int l = valid ? L[me] : -1 - lane;
+  // the warp's kSortTile / 8 labels, loaded once (all in flight together) for both passes;
+  // out-of-range slots get unique negative dummy keys
+  constexpr int RW = kSortTile / 8 / 32;
+  int lbl[RW];
+#pragma unroll
+  for (int r = 0; r < RW; ++r) {
+    const int me = i0 + r * 32 + lane;
+    lbl[r] = me < i1 ? L[me] : -1 - lane;
+  }
+#pragma unroll
+  for (int r = 0; r < RW; ++r) {  // per-warp label counts
+    const int l = lbl[r];
     const unsigned peers = __match_any_sync(0xffffffffu, l);
-    if (valid && __popc(peers & lt) == 0) cw[l] += __popc(peers);
+    if (l >= 0 && __popc(peers & lt) == 0) cw[l] += __popc(peers);
     __syncwarp();
   }
   __syncthreads();
@@ -523,10 +540,11 @@ __global__ void __launch_bounds__(256) k_csort_scatter(const int32_t* __restrict
   }
   __syncthreads();
   int32_t* P = perm + (size_t)bh * N;
-  for (int i = i0; i < i1; i += 32) {
-    const int me = i + lane;
-    const bool valid = me < i1;
-    const int l = valid ? L[me] : -1 - lane;  // unique dummy keys for the tail
+#pragma unroll
+  for (int r = 0; r < RW; ++r) {
+    const int me = i0 + r * 32 + lane;
+    const int l = lbl[r];
+    const bool valid = l >= 0;
     const unsigned peers = __match_any_sync(0xffffffffu, l);
     const int rank = __popc(peers & lt);
     const int basep = valid ? cw[l] : 0;
