@@ -425,13 +425,10 @@ int assign_box_rows(int ks) { return use_pair(ks) ? assign_chunk_n(ks) / 2 : ass
 cudaError_t launch_assign_gemm(const CUtensorMap* tm_x, const CUtensorMap* tm_w, int B, int H, int N,
                                int d, int ks, int nch, int ks_pad, const float* bias, int32_t* labels,
                                cudaStream_t st) {
-  static int num_sms = 0;
-  if (!num_sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (num_sms <= 0) num_sms = 148;
-  }
+  int num_sms = 0, dev = 0;  // queried per call: no shared mutable state, right for any current device
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+  if (num_sms <= 0) num_sms = 148;
   const int units_per_head = (N + asg::TILES * asg::BM - 1) / (asg::TILES * asg::BM);
   const int num_units = units_per_head * B * H;
   if (use_pair(ks)) {
