@@ -628,7 +628,8 @@ def test_layer_cuda_graph_capture_and_replay(pb):
         assert torch.equal(out, ref)
 
 
-def test_batch_of_two_layers(pb):
+@pytest.mark.parametrize("kk", [48, 200])  # 200: the CTA-pair assignment kernel over (b, h) units
+def test_batch_of_two_layers(pb, kk):
     """B = 2: the sampler streams are keyed by b (R4: (b H + h) 2 + side), every kernel indexes
     (b, h) through the strides.  First-iteration labels of batch 1 match the oracle run with b = 1
     (outside near-ties), and each (b, h) output matches the oracle's masked attention on the GPU's
@@ -636,19 +637,19 @@ def test_batch_of_two_layers(pb):
     d = 128
     w = random_qkv(2, 2, 1500, d, seed=61)
     q, k, v = w.q.cuda(), w.k.cuda(), w.v.cuda()
-    st = pb.coclust_assign(q, k, 16, 48, 1, seed=4)
+    st = pb.coclust_assign(q, k, 16, kk, 1, seed=4)
     torch.cuda.synchronize()
     for b in range(2):
         for h in range(2):
-            cc = svoo.cocluster(f64(w.q[b, h]), f64(w.k[b, h]), 16, 48, 1, seed=4, b=b, h=h, H=2)
+            cc = svoo.cocluster(f64(w.q[b, h]), f64(w.k[b, h]), 16, kk, 1, seed=4, b=b, h=h, H=2)
             tk = cc.trace[0]
             ok = tk["gap"] >= GAP_TOL
             assert np.sum((st["lk"][b, h].cpu().numpy() != tk["labels"]) & ok) == 0, (b, h)
     budget = torch.tensor([0.3, 0.5], dtype=torch.float32).cuda()
-    st = pb.coclust_assign(q, k, 16, 48, 2, seed=4)
+    st = pb.coclust_assign(q, k, 16, kk, 2, seed=4)
     n_keep, kept = pb.block_select(st["cq"], st["ck"], st["offs_q"], st["offs_k"], budget, 0.95, 0.1, pb.RULE_DENSITY)
     o = pb.block_sparse_attn(q, k, v, st["perm_q"], st["offs_q"], st["perm_k"], st["offs_k"], n_keep, kept)
-    of = pb.coclust_sparse_attention(q, k, v, 16, 48, 2, budget, seed=4)
+    of = pb.coclust_sparse_attention(q, k, v, 16, kk, 2, budget, seed=4)
     torch.cuda.synchronize()
     assert torch.equal(o, of)
     for b in range(2):
