@@ -1,5 +1,6 @@
-"""Parity at BASELINE.json's full size (Wan2.1-14B 720p: N=75,600, H=40, d=128, 100/500 clusters,
-I_max=2, FIXED rho=0.2) in the launch configuration bench.py times.  The oracle cannot run the
+"""Parity at BASELINE.json's full sizes (Wan2.1-14B 720p: N=75,600, H=40; HunyuanVideo 720p:
+N=118,800, H=24; Wan2.1-1.3B 480p: N=32,760, H=12; d=128, 100/500 clusters, I_max=2, FIXED
+rho=0.2) in the launch configuration bench.py times.  The oracle cannot run the
 whole layer in seconds, so each stage is checked on sampled heads / rows against the oracle fed
 the GPU's own upstream state (teacher forcing), with the SURVEY §8c tolerances."""
 import math
@@ -13,14 +14,13 @@ from oracle import svoo
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
 KQ, KK, IT, BUDGET = 100, 500, 2, 0.2
-HEADS = (0, 23)
 
 
-@pytest.fixture(scope="module")
-def run():
+@pytest.fixture(scope="module", params=["wan14b_720p", "hunyuan_720p", "wan1.3b_480p"])
+def run(request):
     import paper_2603_18636_b200 as pb
     from synthetic import config_workload
-    w = config_workload("wan14b_720p", device="cuda")
+    w = config_workload(request.param, device="cuda")
     H = w.q.shape[1]
     budget = torch.full((H,), BUDGET, device="cuda")
     st = pb.coclust_assign(w.q, w.k, KQ, KK, IT, seed=0)
@@ -28,7 +28,7 @@ def run():
                                    pb.RULE_FIXED)
     o = pb.coclust_sparse_attention(w.q, w.k, w.v, KQ, KK, IT, budget, rule=pb.RULE_FIXED, seed=0)
     torch.cuda.synchronize()
-    return dict(pb=pb, w=w, st=st, n_keep=n_keep, kept=kept, o=o, H=H)
+    return dict(pb=pb, w=w, st=st, n_keep=n_keep, kept=kept, o=o, H=H, heads=(0, H // 2, H - 1))
 
 
 def f64(t):
@@ -40,7 +40,7 @@ def test_fullsize_first_halfstep_labels(run):
     near-ties (gap < 1e-4)."""
     pb, w = run["pb"], run["w"]
     N = w.q.shape[2]
-    for h in HEADS:
+    for h in run["heads"]:
         iq = svoo.sample_anchor_indices(N, KQ, 0, 0, h, run["H"], 0)
         ik = svoo.sample_anchor_indices(N, KK, 0, 0, h, run["H"], 1)
         K = f64(w.k[0, h])
@@ -57,7 +57,7 @@ def test_fullsize_first_halfstep_labels(run):
 
 def test_fullsize_permutation_bitexact(run):
     st = run["st"]
-    for h in HEADS:
+    for h in run["heads"]:
         for side, k in (("q", KQ), ("k", KK)):
             lab = st["l" + side][0, h].cpu().numpy()
             perm, offs = svoo.counting_sort(lab, k)
@@ -67,7 +67,7 @@ def test_fullsize_permutation_bitexact(run):
 
 def test_fullsize_centroids_are_member_means(run):
     st, w = run["st"], run["w"]
-    for h in HEADS[:1]:
+    for h in run["heads"][:2]:
         for side, X, k in (("q", w.q, KQ), ("k", w.k, KK)):
             lab = st["l" + side][0, h].cpu().numpy()
             C = st["c" + side][0, h].cpu().double().numpy()
@@ -110,13 +110,13 @@ def test_fullsize_selection_bitexact(run):
 def test_fullsize_attention_sampled_rows(run):
     st, w, o = run["st"], run["w"], run["o"]
     rng = np.random.default_rng(0)
-    for h in HEADS:
+    for h in run["heads"]:
         Lq = st["lq"][0, h].cpu().numpy()
         Lk = st["lk"][0, h].cpu().numpy()
         n = int(run["n_keep"][0, h])
         kept = run["kept"][0, h, :, :n].cpu().numpy()
         Q, K, V = f64(w.q[0, h]), f64(w.k[0, h]), f64(w.v[0, h])
-        rows = rng.choice(Q.shape[0], 192, replace=False)
+        rows = rng.choice(Q.shape[0], 384, replace=False)
         ref = np.stack([_row(Q, K, V, Lq, Lk, kept, i) for i in rows])
         got = f64(o[0, h])[rows]
         err = np.abs(got - ref)
