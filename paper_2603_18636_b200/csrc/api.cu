@@ -223,6 +223,17 @@ cs_status make_map_x(CUtensorMap* m, cs_bf16_in x, int B, int H, int N, int d) {
   return CS_OK;
 }
 
+// Stage events: a plain record outside stream capture; while the stream is being captured into a
+// CUDA graph, an external event-record node, so the event still times the stage in every replay.
+static cudaError_t record_stage_event(void* ev, cudaStream_t st) {
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaError_t e = cudaStreamIsCapturing(st, &cap);
+  if (e != cudaSuccess) return e;
+  return cap == cudaStreamCaptureStatusActive
+             ? cudaEventRecordWithFlags(static_cast<cudaEvent_t>(ev), st, cudaEventRecordExternal)
+             : cudaEventRecord(static_cast<cudaEvent_t>(ev), st);
+}
+
 // ---------------------------------------------------------------- launch sequences
 cs_status run_assign_step(int B, int H, int N, int d, cs_bf16_in x, int ka, const float* ca, int ks,
                           const float* cself, int32_t* labels, const AssignScratch& sc, cudaStream_t st) {
@@ -286,7 +297,7 @@ cs_status run_attn(int B, int H, int N, int d, int kq, int kk, const int32_t* pe
     CS_CHECK(make_map_2d(&kv.k[i], sc.kp, (uint64_t)BH * N, d, 8u << i));
     CS_CHECK(make_map_2d(&kv.v[i], sc.vp, (uint64_t)BH * N, d, 8u << i));
   }
-  if (ev) CS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(ev[2]), st), "event");
+  if (ev) CS_CUDA(record_stage_event(ev[2], st), "event");
   // opt-in persistent attention kernel (attn_persist.cu; measured neutral on Wan14B / Wan1.3B)
   const bool persist = getenv("CS_ATTN_PERSIST") != nullptr;
   if (persist)
@@ -303,7 +314,7 @@ cs_status run_attn(int B, int H, int N, int d, int kq, int kk, const int32_t* pe
                            po ? po->s_tok : o.sn, po ? static_cast<const uint64_t*>(po->ptrs) : nullptr,
                            po ? po->n_per_rank : 0, po ? po->head_base : 0, st),
             "bsa_fwd");
-  if (ev) CS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(ev[3]), st), "event");
+  if (ev) CS_CUDA(record_stage_event(ev[3], st), "event");
   return CS_OK;
 }
 
@@ -548,18 +559,18 @@ cs_status run_layer(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in k, cs_b
     CS_CHECK(run_assign(B, H, N, d, q, k, kq, kk, iters, seed, head_offset, heads_total, nullptr, nullptr, s.cq,
                         s.ck, s.lq, s.lk, s.perm_q, s.offs_q, s.perm_k, s.offs_k, as, at.qp, at.kp, st,
                         (sel_flags & CS_CLUSTER_KMEANS) != 0));
-    if (ev) CS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(ev[0]), st), "event");
+    if (ev) CS_CUDA(record_stage_event(ev[0], st), "event");
     CS_CUDA(launch_block_select(BH, H, kq, kk, d, s.cq, s.ck, s.offs_q, s.offs_k, budget, tau, theta, rule,
                                 sel_flags & (CS_SEL_PER_ROW | CS_SEL_SIZE_WEIGHTED), s.n_keep, s.n_rows, s.kept,
                                 se.order, se.cnt, se.abar, st),
             "block_select");
-    if (ev) CS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(ev[1]), st), "event");
+    if (ev) CS_CUDA(record_stage_event(ev[1], st), "event");
   } else {
     // clustering reuse across denoising steps: only the permuted copies are new
-    if (ev) CS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(ev[0]), st), "event");
+    if (ev) CS_CUDA(record_stage_event(ev[0], st), "event");
     CS_CUDA(launch_permute_rows(view(q, H), BH, N, d, s.perm_q, at.qp, st), "permute_q");
     CS_CUDA(launch_permute_rows(view(k, H), BH, N, d, s.perm_k, at.kp, st), "permute_k");
-    if (ev) CS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(ev[1]), st), "event");
+    if (ev) CS_CUDA(record_stage_event(ev[1], st), "event");
   }
   CS_CUDA(launch_permute_rows(view(v, H), BH, N, d, s.perm_k, at.vp, st), "permute_v");
   return run_attn(B, H, N, d, kq, kk, s.perm_q, s.offs_q, s.offs_k, s.n_keep, s.n_rows, s.kept, scale, o, at, st,
