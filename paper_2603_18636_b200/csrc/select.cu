@@ -68,54 +68,57 @@ __device__ void bitonic_sort_rows(double (&v)[E], int (&ix)[E], int P2, double* 
   __syncthreads();
 }
 
-// Abar = C_q C_k^T in fp64.  grid (ceil(kk/64), ceil(kq/32), BH), block 256, dyn smem
-// (32 + 64) x (D+1) doubles: a 32 x 64 output tile; thread (ta, tj) = (t / 16, t % 16) owns the
-// outputs (a0 + ta + 16 i, j0 + tj + 16 jj), i < 2, jj < 4, each a dot product of length D in a
-// fixed (sequential) order.  Rows padded to D+1 doubles: the 16 lanes of a half-warp hit 16
-// distinct bank pairs.
+// Abar = C_q C_k^T in fp64.  grid (ceil(kk/64), ceil(kq/64), BH), block 256, dyn smem
+// 2 x 64 x (64+1) doubles: a 64 x 64 output tile; thread (ta, tj) = (t / 16, t % 16) owns the
+// outputs (a0 + ta + 16 i, j0 + tj + 16 jj), i, jj < 4, each a dot product of length D in a fixed
+// (sequential) order, the D columns staged through SMEM in chunks of 64.  Rows padded to 65
+// doubles: the 16 lanes of a half-warp hit 16 distinct bank pairs; 8 SMEM wavefronts per 16 DFMA.
 template <int D>
 __global__ void __launch_bounds__(256) k_abar(int kq, int kk, const float* __restrict__ cq,
                                               const float* __restrict__ ck, double* __restrict__ abar) {
-  constexpr int TA = 32, TJ = 64, LD = D + 1;
+  constexpr int TA = 64, TJ = 64, EC = 64, LD = EC + 1;
   extern __shared__ double sm_ab[];
   double* sq = sm_ab;             // [TA][LD]
   double* sk = sm_ab + TA * LD;   // [TJ][LD]
   const int bh = blockIdx.z, a0 = blockIdx.y * TA, j0 = blockIdx.x * TJ, t = threadIdx.x;
-  for (int i = t; i < TA * D / 4; i += 256) {
-    const int r = i / (D / 4), c = (i % (D / 4)) * 4;
-    const float4 v = (a0 + r < kq) ? *reinterpret_cast<const float4*>(cq + ((size_t)bh * kq + a0 + r) * D + c)
-                                   : make_float4(0.f, 0.f, 0.f, 0.f);
-    double* d = sq + r * LD + c;
-    d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
-  }
-  for (int i = t; i < TJ * D / 4; i += 256) {
-    const int r = i / (D / 4), c = (i % (D / 4)) * 4;
-    const float4 v = (j0 + r < kk) ? *reinterpret_cast<const float4*>(ck + ((size_t)bh * kk + j0 + r) * D + c)
-                                   : make_float4(0.f, 0.f, 0.f, 0.f);
-    double* d = sk + r * LD + c;
-    d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
-  }
-  __syncthreads();
   const int ta = t >> 4, tj = t & 15;
-  double acc[2][4];
+  double acc[4][4];
 #pragma unroll
-  for (int i = 0; i < 2; ++i)
+  for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int jj = 0; jj < 4; ++jj) acc[i][jj] = 0.0;
+  for (int e0 = 0; e0 < D; e0 += EC) {
+    if (e0) __syncthreads();
+    for (int i = t; i < TA * EC / 4; i += 256) {
+      const int r = i / (EC / 4), c = (i % (EC / 4)) * 4;
+      const float4 v = (a0 + r < kq) ? *reinterpret_cast<const float4*>(cq + ((size_t)bh * kq + a0 + r) * D + e0 + c)
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+      double* d = sq + r * LD + c;
+      d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
+    }
+    for (int i = t; i < TJ * EC / 4; i += 256) {
+      const int r = i / (EC / 4), c = (i % (EC / 4)) * 4;
+      const float4 v = (j0 + r < kk) ? *reinterpret_cast<const float4*>(ck + ((size_t)bh * kk + j0 + r) * D + e0 + c)
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+      double* d = sk + r * LD + c;
+      d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
+    }
+    __syncthreads();
 #pragma unroll 4
-  for (int e = 0; e < D; ++e) {
-    double qv[2], kv[4];
+    for (int e = 0; e < EC; ++e) {
+      double qv[4], kv[4];
 #pragma unroll
-    for (int i = 0; i < 2; ++i) qv[i] = sq[(ta + 16 * i) * LD + e];
+      for (int i = 0; i < 4; ++i) qv[i] = sq[(ta + 16 * i) * LD + e];
 #pragma unroll
-    for (int jj = 0; jj < 4; ++jj) kv[jj] = sk[(tj + 16 * jj) * LD + e];
+      for (int jj = 0; jj < 4; ++jj) kv[jj] = sk[(tj + 16 * jj) * LD + e];
 #pragma unroll
-    for (int i = 0; i < 2; ++i)
+      for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int jj = 0; jj < 4; ++jj) acc[i][jj] = fma(qv[i], kv[jj], acc[i][jj]);
+        for (int jj = 0; jj < 4; ++jj) acc[i][jj] = fma(qv[i], kv[jj], acc[i][jj]);
+    }
   }
 #pragma unroll
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < 4; ++i) {
     const int a = a0 + ta + 16 * i;
     if (a >= kq) continue;
     double* row = abar + ((size_t)bh * kq + a) * kk;
@@ -348,14 +351,13 @@ cudaError_t launch_block_select(int BH, int H, int kq, int kk, int d, const floa
   int P2 = 256;
   while (P2 < kk) P2 <<= 1;
   const size_t smem = (size_t)P2 * 8 + (size_t)d * 8 + (size_t)P2 * 4;
-  const dim3 gab((kk + 63) / 64, (kq + 31) / 32, BH);
+  const dim3 gab((kk + 63) / 64, (kq + 63) / 64, BH);
+  constexpr int sab = 2 * 64 * 65 * 8;  // > 48 KB: opt in
   if (d == 128) {
-    constexpr int sab = (32 + 64) * 129 * 8;
     cudaError_t e = cudaFuncSetAttribute(k_abar<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, sab);
     if (e != cudaSuccess) return e;
     k_abar<128><<<gab, 256, sab, st>>>(kq, kk, cq, ck, abar);
   } else {
-    constexpr int sab = (32 + 64) * 65 * 8;  // > 48 KB as well
     cudaError_t e = cudaFuncSetAttribute(k_abar<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, sab);
     if (e != cudaSuccess) return e;
     k_abar<64><<<gab, 256, sab, st>>>(kq, kk, cq, ck, abar);
