@@ -10,19 +10,27 @@ the readings the paper leaves open, the DESIGN.md reading ids R1..R17 (which res
 SURVEY.md §8c).  Inputs are the exact bf16 values the GPU path also consumes, widened to fp64.
 
 Functions and their pins (tests/test_oracle_*.py):
-  splitmix64_next / sample_anchor_indices   R4            pinned: published splitmix64 vectors,
+  splitmix64_next / sample_anchor_indices   R4            pinned: published splitmix64 vectors
+                                                          (seeds 0 and 1234567), literal stream
+                                                          seeds and Floyd draws derived by hand,
                                                           distinctness/range/uniformity
   l2_normalize_rows, softmax_row                           pinned: SPEC worked examples (golden)
   assign_step (Alg.1 Step A/B assignment)   P:1214-1226   pinned: cosine nearest-centroid special
                                                           case, brute-force 2-partition, K=1,
-                                                          explicit-difference distances
+                                                          explicit-difference distances, closed-
+                                                          form gap (unsquared distances)
   update_centroids (Alg.1 Mean)             P:1219,1227   pinned: member-mean / sum invariants
-  cocluster (Alg.1)                         P:1203-1229   pinned only by invariants (token-order
-                                                          invariance, optimality snapshot) —
-                                                          "parity unpinned" end to end: the paper
-                                                          prints no worked example.
+  cocluster (Alg.1)                         P:1203-1229   pinned: hand-derived 2-D examples
+                                                          (tests/golden/alg1_examples.json): the
+                                                          Fig. 3 coupling construction,
+                                                          two full iterations with the centroid
+                                                          generation of every half-step and the
+                                                          returned (post-update, R13) centroids;
+                                                          token-order invariance; R13 member means
   counting_sort                             implied P:1266 pinned: np.argsort(kind="stable")
-  select_blocks (Ā, Recall, ρ rule, top-ρK)  P:1247-1257   pinned: SPEC worked examples, nesting;
+  select_blocks (Ā, Recall, ρ rule, top-ρK)  P:1247-1257   pinned: SPEC worked examples, nesting,
+                                                          hand examples of n_rec (ceil over K_q')
+                                                          and of both DENSITY branches;
     + NEXT-4 variants (per_row, size_weighted)            pinned: reduce to the base reading
                                                           (FIXED / equal sizes), closed-form
                                                           size-weighted masses, hand example
@@ -125,6 +133,9 @@ def assign_step(X: np.ndarray, C_anchor: np.ndarray, C_self: np.ndarray) -> Assi
     Norm = row L2 (R1), normalisation applied to the final affinity rows (R3), ties -> lowest j (R2).
     The Euclidean distance is evaluated as sqrt(|a|^2 + |b|^2 - 2 a.b) with a matmul for the
     cross term (a library primitive used as a step); tests check it against explicit differences.
+    |a|^2 of a Norm'ed row is exactly 1 (0 for a zero row, R1) and is used as such, so a zero
+    affinity row is at distance exactly 1 from every nonzero row and its tie goes to the lowest j
+    (R2) instead of being decided by the last ulp of a rounded |b|^2.
     """
     X = np.asarray(X, np.float64)
     Ca = np.asarray(C_anchor, np.float64)
@@ -133,7 +144,9 @@ def assign_step(X: np.ndarray, C_anchor: np.ndarray, C_self: np.ndarray) -> Assi
     Pbar = Cs @ Ca.T                  # affinity of each self centroid to anchors   [K_s, K_a]
     Ph = l2_normalize_rows(P)
     Pbh = l2_normalize_rows(Pbar)
-    sq = (Ph * Ph).sum(1)[:, None] + (Pbh * Pbh).sum(1)[None, :] - 2.0 * (Ph @ Pbh.T)
+    na = np.any(P != 0, axis=1).astype(np.float64)      # |P^_i|^2 in {0, 1}
+    nb = np.any(Pbar != 0, axis=1).astype(np.float64)   # |Pbar^_j|^2 in {0, 1}
+    sq = na[:, None] + nb[None, :] - 2.0 * (Ph @ Pbh.T)
     D = np.sqrt(np.maximum(sq, 0.0))  # [N, K_s]
     labels = np.argmin(D, axis=1)     # first minimum -> lowest index on ties
     N, Ks = D.shape
