@@ -58,8 +58,6 @@ def parse():
                          "(fused, CUDA IPC / NVLink) or NCCL all_to_all + unpack")
     ap.add_argument("--graph", choices=["on", "off"], default="on",
                     help="time the layer as CUDA-graph replays (one captured layer call; head-parallel)")
-    ap.add_argument("--cpu-sample-rows", type=int, default=1500,
-                    help="query rows of the oracle attention sample")
     return ap.parse_args()
 
 
@@ -131,62 +129,94 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------ oracle baseline
-def cpu_oracle_sample(w, h, kq, kk, iters, budget, rule, tau, theta, seed, H_total, rows):
-    """Time the float64 oracle on one head: full co-clustering + selection, attention on a row
-    sample; returns (extrapolated ms per layer, details)."""
-    import numpy as np
-    from oracle import svoo
-    f = lambda t: t.float().cpu().double().numpy()
-    Q, K, V = f(w.q[0, h]), f(w.k[0, h]), f(w.v[0, h])
-    N, d = Q.shape
-    t0 = time.perf_counter()
-    cc = svoo.cocluster(Q, K, kq, kk, iters, seed=seed, h=h, H=H_total)
-    pq, oq = svoo.counting_sort(cc.Lq, kq)
-    pk, ok = svoo.counting_sort(cc.Lk, kk)
-    sel = svoo.select_blocks(cc.Cq, cc.Ck, np.diff(oq), np.diff(ok), budget, tau, theta, rule, d_head=d)
-    t1 = time.perf_counter()
-    rs = np.random.default_rng(0).choice(N, size=min(rows, N), replace=False)
-    Lq, Lk = cc.Lq, cc.Lk
-    t2 = time.perf_counter()
-    for a in np.unique(Lq[rs]):
-        rr = rs[Lq[rs] == a]
-        svoo.sparse_attention(Q[rr], K, V, np.zeros(len(rr), np.int64), Lk, {0: sel.kept[a]})
-    t3 = time.perf_counter()
-    per_head_s = (t1 - t0) + (t3 - t2) * N / len(rs)
-    return per_head_s * H_total * 1e3, dict(cluster_s=t1 - t0, attn_sample_s=t3 - t2, rows=len(rs))
+# the float64 oracle timed on this host's cores on ONE COMPLETE HEAD of the workload
+# (co-clustering, selection, and the attention of every one of the N query rows, grouped by query
+# cluster as the oracle computes it), extrapolated x H to ms per layer (every head costs the same
+# work up to its cluster sizes).  The cpu_baseline leg and the --impl reference arm time the same
+# head with the same code; the reference arm spreads the head's attention over its K steps (step
+# i = the query clusters a = i mod K) so each step is a bounded sample and no row is extrapolated.
+class OracleHead:
+    def __init__(self, w, h, kq, kk, iters, budget, rule, tau, theta, seed, H_total):
+        import numpy as np
+        from oracle import svoo
+        f = lambda t: t.float().cpu().double().numpy()
+        self.Q, self.K, self.V = f(w.q[0, h]), f(w.k[0, h]), f(w.v[0, h])
+        self.args = (kq, kk, iters, budget, rule, tau, theta, seed, h, H_total)
+        self.np, self.svoo = np, svoo
+
+    def cluster(self):
+        """Alg. 1 + counting sort + selection (timed)."""
+        np, svoo = self.np, self.svoo
+        kq, kk, iters, budget, rule, tau, theta, seed, h, H_total = self.args
+        t0 = time.perf_counter()
+        cc = svoo.cocluster(self.Q, self.K, kq, kk, iters, seed=seed, h=h, H=H_total)
+        _, oq = svoo.counting_sort(cc.Lq, kq)
+        _, ok = svoo.counting_sort(cc.Lk, kk)
+        self.sel = svoo.select_blocks(cc.Cq, cc.Ck, np.diff(oq), np.diff(ok), budget, tau, theta, rule,
+                                      d_head=self.Q.shape[1])
+        self.Lq, self.Lk = cc.Lq, cc.Lk
+        return time.perf_counter() - t0
+
+    def attention(self, clusters):
+        """The oracle's masked-softmax attention for all rows of the given query clusters (timed)."""
+        np, svoo = self.np, self.svoo
+        t0 = time.perf_counter()
+        for a in clusters:
+            rows = np.nonzero(self.Lq == a)[0]
+            if rows.size:
+                svoo.sparse_attention(self.Q[rows], self.K, self.V, np.full(rows.size, a), self.Lk, self.sel.kept)
+        return time.perf_counter() - t0
+
+
+def oracle_sample_text(H, N, kq, kk, iters, detail=""):
+    return (f"one complete head of {H} (float64 oracle: Alg. 1 with {iters} iterations at {kq}/{kk} clusters, "
+            f"selection, and the masked-softmax attention of all {N} query rows grouped by query cluster)"
+            f"{detail}; value = per-head time x {H} heads (extrapolation over heads only)")
+
+
+def bench_config(args, H, N, d, world, mode, tensor_bytes):
+    """The config dict of both arms (identical for the same workload)."""
+    return {"workload": CONFIG_NAMES[args.config], "B": 1, "H": H, "N": N, "d": d,
+            "kq": args.kq, "kk": args.kk, "iters": args.iters, "budget": args.budget,
+            "rule": args.rule, "tau": args.tau, "theta": args.theta, "sel_flags": args.sel_flags,
+            "parallelism": (f"ulysses-a2a x{world} (return: {args.ulysses_return})" if mode == "ulysses"
+                            else f"head-parallel x{world}"),
+            "l2": "inputs larger than L2 (%.0f MB/tensor/rank)" % (tensor_bytes / 1e6)}
 
 
 def run_reference(args):
-    """--impl reference: the float64 oracle as it stands, on this host's cores."""
-    import torch
+    """--impl reference: the float64 oracle as it stands, on this host's cores (rank 0 only)."""
     from synthetic import CONFIGS, video_qkv
     world, rank, local = dist_init(args)
     if rank != 0:
         return
     c = CONFIGS[args.config]
-    H = c["H"]
-    w = video_qkv(c["T"], c["Hs"], c["Ws"], 1, c["d"], seed=args.seed, layer=0)  # head 0 stream
+    H, d = c["H"], c["d"]
+    w = video_qkv(c["T"], c["Hs"], c["Ws"], 1, d, seed=args.seed, layer=0)  # = head 0 of the layer
+    N = w.q.shape[2]
     cores = len(os.sched_getaffinity(0))
-    rows = max(64, args.cpu_sample_rows // 3)
-    for _ in range(args.warmup):
-        cpu_oracle_sample(w, 0, args.kq, args.kk, 1, args.budget, RULES[args.rule], args.tau, args.theta,
-                          args.seed, H, 64)
-    vals = []
-    for _ in range(args.steps):
-        v, det = cpu_oracle_sample(w, 0, args.kq, args.kk, args.iters, args.budget, RULES[args.rule],
-                                   args.tau, args.theta, args.seed, H, rows)
-        vals.append(v)
-    ms = sum(vals) / len(vals)
-    N, d = w.q.shape[2], w.q.shape[3]
-    sample = (f"1 of {H} heads: full co-clustering ({args.iters} it, {args.kq}/{args.kk}) + selection, "
-              f"attention on {rows} random query rows; extrapolated x N/rows x H")
+    head = OracleHead(w, 0, args.kq, args.kk, args.iters, args.budget, RULES[args.rule], args.tau, args.theta,
+                      args.seed, H)
+    t_cluster = head.cluster()                         # the head's clustering + selection, timed once
+    for i in range(args.warmup):                       # warm-up: one (small) query cluster each
+        head.attention([i % args.kq])
+    K = args.steps
+    t_steps = [head.attention(range(i, args.kq, K)) for i in range(K)]   # together: every row once
+    head_s = t_cluster + sum(t_steps)
+    ms = head_s * H * 1e3
+    mode = args.parallel or ("ulysses" if (args.config == "hunyuan_720p" and world > 1) else "head")
+    hl = H // world if mode == "ulysses" else (lambda r: r[1] - r[0])(head_range(H, world, 0))
     line = {"impl": "reference", "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
+            "steps": K, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "dense_equiv_tflops": 4.0 * H * N * N * d / (ms * 1e-3) / 1e12,
-            "config": {"workload": CONFIG_NAMES[args.config], "H": H, "N": N, "d": d, "kq": args.kq,
-                       "kk": args.kk, "iters": args.iters, "budget": args.budget, "rule": args.rule},
-            "cpu_baseline": {"value": ms, "unit": "ms", "cores": cores, "kind": "oracle", "sample": sample},
+            "config": bench_config(args, H, N, d, world, mode, hl * N * d * 2),
+            "value_kind": "extrapolated over heads: one complete head timed, x H",
+            "oracle_head_s": {"cluster_select": t_cluster, "attention": sum(t_steps)},
+            "cpu_baseline": {"value": ms, "unit": "ms", "cores": cores, "kind": "oracle",
+                             "sample": oracle_sample_text(H, N, args.kq, args.kk, args.iters,
+                                                          f"; attention split over the {K} steps (step i = "
+                                                          f"query clusters i mod {K})")},
             "e2e": {"value": ms, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -454,24 +484,20 @@ def run_ours(args):
     dense_flops = 4.0 * B * H_total * N * N * d
     cpu = None
     if not args.no_cpu_baseline and world == 1:
-        v_ms, det = cpu_oracle_sample(cpu_src, 0, args.kq, args.kk, args.iters, args.budget, rule, args.tau,
-                                      args.theta, args.seed, H_total, args.cpu_sample_rows)
-        cpu = {"value": v_ms, "unit": "ms", "cores": len(os.sched_getaffinity(0)), "kind": "oracle",
-               "sample": (f"head 0 of {H_total}: full float64 co-clustering ({args.iters} it, {args.kq}/"
-                          f"{args.kk}) + selection ({det['cluster_s']:.1f} s) and attention on "
-                          f"{det['rows']} random query rows ({det['attn_sample_s']:.1f} s); "
-                          f"extrapolated x N/rows, x H (ms per layer)")}
+        head = OracleHead(cpu_src, 0, args.kq, args.kk, args.iters, args.budget, rule, args.tau, args.theta,
+                          args.seed, H_total)
+        t_c = head.cluster()
+        t_a = head.attention(range(args.kq))
+        cpu = {"value": (t_c + t_a) * H_total * 1e3, "unit": "ms", "cores": len(os.sched_getaffinity(0)),
+               "kind": "oracle", "value_kind": "extrapolated over heads: one complete head timed, x H",
+               "sample": oracle_sample_text(H_total, N, args.kq, args.kk, args.iters,
+                                            f" ({t_c:.1f} s clustering + selection, {t_a:.1f} s attention)")}
     line = {
         "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world, "steps": K, "warmup": args.warmup,
         "ms_per_step": ms, "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic",
         "dense_equiv_tflops": dense_flops / (ms * 1e-3) / 1e12,
-        "config": {"workload": CONFIG_NAMES[args.config], "B": B, "H": H_total, "N": N, "d": d,
-                   "kq": args.kq, "kk": args.kk, "iters": args.iters, "budget": args.budget,
-                   "rule": args.rule, "tau": args.tau, "theta": args.theta, "sel_flags": args.sel_flags,
-                   "parallelism": (f"ulysses-a2a x{world} (return: {args.ulysses_return})" if mode == "ulysses"
-                                   else f"head-parallel x{world}"),
-                   "l2": "inputs larger than L2 (%.0f MB/tensor/rank)" % (q.numel() * 2 / 1e6)},
+        "config": bench_config(args, H_total, N, d, world, mode, q.numel() * 2),
         "kept_tflop_per_layer": f_kept_total / 1e12,
         "kept_frac": f_kept_total / dense_flops,
         "stages_ms": {"cocluster": st_cluster, "select": st_select, "permute_v_worklist": st_prep,

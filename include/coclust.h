@@ -15,13 +15,15 @@
  * - Q, K, V, O are bf16 [B, H, N, d] given as (ptr, sb, sh, sn): element strides of the B, H and N
  *   dimensions; the d dimension must be contiguous (stride 1).  Both [B,H,N,d] and [B,N,H,d]
  *   buffers are expressible.  d must be 64 or 128.  ptr must be 16-byte aligned and sb, sh, sn
- *   multiples of 8 elements (TMA).
+ *   multiples of 8 elements (TMA); broadcast views (stride 0 over an extent > 1) and overlapping
+ *   rows (sn < d with N > 1) are rejected with CS_ERR_SHAPE.
  * - "bh" below is b*H + h.  Labels are int32 in [0, k).  perm[bh][p] = the token at cluster-sorted
  *   position p (stable: ascending token index inside a cluster); offs[bh][c]..offs[bh][c+1] are the
  *   positions of cluster c (offs[bh][0] = 0, offs[bh][k] = N).
  * - Centroids are fp32 [B, H, k, d] contiguous.
- * - ws / ws_bytes: caller-owned scratch of at least cs_workspace_bytes(...) bytes, 256-byte
- *   aligned.  Its contents are undefined between calls.
+ * - ws / ws_bytes: caller-owned scratch of at least cs_workspace_bytes(...) bytes, 16-byte
+ *   aligned (CS_ERR_ALIGN otherwise; the library rounds the base up to 256 bytes inside the
+ *   slack cs_workspace_bytes includes).  Its contents are undefined between calls.
  * - Errors: arguments are validated on the host BEFORE anything is enqueued; on error nothing is
  *   launched and a cs_status != CS_OK is returned; cs_last_error() (thread-local) holds a message.
  *   CS_ERR_CUDA reports a launch error; asynchronous device faults surface at the caller's next
@@ -42,7 +44,8 @@ extern "C" {
 typedef enum {
   CS_OK = 0,
   CS_ERR_NULL = 1,        /* a required pointer is NULL                                       */
-  CS_ERR_SHAPE = 2,       /* B,H,N <= 0, d not in {64,128}, inconsistent strides               */
+  CS_ERR_SHAPE = 2,       /* B,H,N <= 0, d not in {64,128}, inconsistent strides: a stride of 0
+                             on a dimension of extent > 1 (broadcast) or sn < d (overlapping rows) */
   CS_ERR_ARG = 3,         /* k > N or k > 1024, iters < 1, tau not in (0,1], theta not in (0,1),
                              scale <= 0, unknown rule                                           */
   CS_ERR_ALIGN = 4,       /* pointer not 16-byte aligned or stride not a multiple of 8 elements */
@@ -168,11 +171,13 @@ cs_status block_select_ex(int B, int H, int kq, int kk, int d, const float* cq, 
                           int32_t* n_keep_rows, int32_t* kept, void* ws, size_t ws_bytes,
                           void* stream);
 
-/* Block-sparse attention over the kept blocks.  (Environment CS_ATTN_PERSIST=1 selects the
- * bit-identical persistent variant of the kernel, one CTA per SM over the work items.)
+/* Block-sparse attention over the kept blocks.
  *   for query i in cluster a: o_i = sum_{j: L_k(j) in kept[a]} softmax_j(q_i.k_j * scale) v_j,
  * written in ORIGINAL token order (the inverse permutation is fused into the stores).  bf16 MMA,
- * fp32 accumulation and softmax, bf16 P (R15).  scale > 0 (1/sqrt(d) for the paper). */
+ * fp32 accumulation and softmax, bf16 P (R15).  scale > 0 (1/sqrt(d) for the paper).
+ * A caller-supplied kept row whose clusters are all empty (no allowed key: the softmax over an
+ * empty set, S:419's contract violation) gives o_i = 0 for the queries of that row; block_select
+ * never produces such a row (n_keep >= 1 over nonempty key clusters only). */
 cs_status block_sparse_attn(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in k, cs_bf16_in v,
                             int kq, int kk, const int32_t* perm_q, const int32_t* offs_q,
                             const int32_t* perm_k, const int32_t* offs_k, const int32_t* n_keep,

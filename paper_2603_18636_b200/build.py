@@ -20,7 +20,7 @@ ROOT = os.path.dirname(HERE)
 VARIANT = os.environ.get("CS_VARIANT", "")
 LIB = os.path.join(HERE, f"libcoclust_{VARIANT}.so" if VARIANT else "libcoclust.so")
 BUILD = os.path.join(HERE, f"_build_{VARIANT}" if VARIANT else "_build")
-SOURCES = ["api.cu", "cluster.cu", "assign.cu", "select.cu", "attn.cu", "attn_persist.cu", "profile.cu", "peer.cu"]
+SOURCES = ["api.cu", "cluster.cu", "assign.cu", "select.cu", "attn.cu", "profile.cu", "peer.cu"]
 HEADERS = ["common.cuh", "kernels.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",

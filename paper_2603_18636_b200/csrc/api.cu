@@ -2,12 +2,14 @@
 // carving, TMA descriptor encoding and the launch sequences.  No entry point allocates, frees or
 // synchronises; every launch goes to the caller's stream.
 #include <cuda.h>
+#include <nvtx3/nvToolsExt.h>
 #include <stdarg.h>
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
+#include <mutex>
 
 #include "../../include/coclust.h"
 #include "kernels.cuh"
@@ -39,11 +41,21 @@ cs_status cuda_fail(cudaError_t e, const char* where) {
     if (_s != CS_OK) return _s;    \
   } while (0)
 
+// NVTX ranges around the host-side enqueue of each stage (SURVEY §5 per-stage markers: visible to
+// nsys / `ncu --nvtx --nvtx-include`); header-only NVTX3, a no-op unless a tool is attached.
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+};
+
 // ---------------------------------------------------------------- workspace carving
 struct Carve {
   uint8_t* base;  // nullptr -> sizing pass
   size_t off = 0;
-  explicit Carve(void* b) : base(static_cast<uint8_t*>(b)) {}
+  // the base is rounded up to 256 bytes (every need_* adds 256 bytes of slack for this), so a
+  // 16-byte-aligned caller workspace still gives 256-byte-aligned scratch arrays
+  explicit Carve(void* b)
+      : base(b ? reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(b) + 255) & ~uintptr_t(255)) : nullptr) {}
   template <typename T>
   T* take(size_t count) {
     off = (off + 255) & ~size_t(255);
@@ -158,17 +170,30 @@ cs_status check_k(int k, int N, const char* name) {
     return fail(CS_ERR_ARG, "%s must be in [1, min(N, %d)] (got %d, N=%d)", name, kMaxClusters, k, N);
   return CS_OK;
 }
-cs_status check_bf16(const void* ptr, int64_t sb, int64_t sh, int64_t sn, const char* name) {
+// A [B, H, N, d] bf16 operand: 16-byte aligned, strides non-negative multiples of 8 elements, and
+// no dimension of extent > 1 broadcast (stride 0) or rows overlapping (sn < d): every kernel reads
+// the same element for a given (b, h, n) — the TMA maps and the pointer-arithmetic views alike.
+cs_status check_bf16(const void* ptr, int64_t sb, int64_t sh, int64_t sn, int B, int H, int N, int d,
+                     const char* name) {
   if (!ptr) return fail(CS_ERR_NULL, "%s.ptr is NULL", name);
   if (reinterpret_cast<uintptr_t>(ptr) % 16) return fail(CS_ERR_ALIGN, "%s.ptr not 16-byte aligned", name);
   if (sb < 0 || sh < 0 || sn < 0) return fail(CS_ERR_SHAPE, "%s strides must be non-negative", name);
   if (sb % 8 || sh % 8 || sn % 8)
     return fail(CS_ERR_ALIGN, "%s strides must be multiples of 8 elements (got %lld, %lld, %lld)", name,
                 (long long)sb, (long long)sh, (long long)sn);
+  if ((B > 1 && sb == 0) || (H > 1 && sh == 0) || (N > 1 && sn < d))
+    return fail(CS_ERR_SHAPE, "%s: broadcast (stride 0) or overlapping rows (sn < d) are not supported "
+                "(strides %lld, %lld, %lld for B=%d, H=%d, N=%d, d=%d)", name, (long long)sb, (long long)sh,
+                (long long)sn, B, H, N, d);
   return CS_OK;
+}
+template <typename T>
+cs_status check_t(const T& t, int B, int H, int N, int d, const char* name) {
+  return check_bf16(t.ptr, t.sb, t.sh, t.sn, B, H, N, d, name);
 }
 cs_status check_ws(void* ws, size_t have, size_t need) {
   if (!ws) return fail(CS_ERR_WORKSPACE, "workspace is NULL (need %zu bytes)", need);
+  if (reinterpret_cast<uintptr_t>(ws) % 16) return fail(CS_ERR_ALIGN, "workspace not 16-byte aligned");
   if (have < need) return fail(CS_ERR_WORKSPACE, "workspace too small: %zu < %zu bytes", have, need);
   return CS_OK;
 }
@@ -182,16 +207,22 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
                                   CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
                                   CUtensorMapFloatOOBfill);
-EncodeTiledFn encode_fn() {
-  static EncodeTiledFn fn = nullptr;
-  if (!fn) {
+// Driver entry points are resolved once per process (std::call_once: thread-safe); the resolved
+// pointer is immutable afterwards, so the calls stay reentrant.
+void* driver_entry(const char* name, std::once_flag& once, void*& slot) {
+  std::call_once(once, [&] {
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeTiledFn>(p);
-  }
-  return fn;
+    if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) == cudaSuccess && q == cudaDriverEntryPointSuccess)
+      slot = p;
+  });
+  return slot;
+}
+std::once_flag g_encode_once, g_attr_once;
+void* g_encode_fn = nullptr;
+void* g_attr_fn = nullptr;
+EncodeTiledFn encode_fn() {
+  return reinterpret_cast<EncodeTiledFn>(driver_entry("cuTensorMapEncodeTiled", g_encode_once, g_encode_fn));
 }
 // 2D bf16 map over a row-major [rows, cols] matrix, box {64, box_rows}, SWIZZLE_128B.
 cs_status make_map_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
@@ -212,8 +243,12 @@ cs_status make_map_x(CUtensorMap* m, cs_bf16_in x, int B, int H, int N, int d) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return fail(CS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (no CUDA driver?)");
   cuuint64_t dims[4] = {(cuuint64_t)d, (cuuint64_t)N, (cuuint64_t)H, (cuuint64_t)B};
-  cuuint64_t strides[3] = {(cuuint64_t)x.sn * 2, (cuuint64_t)std::max<int64_t>(x.sh, 8) * 2,
-                           (cuuint64_t)std::max<int64_t>(x.sb, 8) * 2};
+  // real strides; only a dimension of extent 1 (never stepped over) may carry a placeholder
+  // (check_bf16 rejects stride 0 on any dimension of extent > 1)
+  const int64_t sn = N > 1 ? x.sn : std::max<int64_t>(x.sn, 8);
+  const int64_t sh = H > 1 ? x.sh : std::max<int64_t>(x.sh, 8);
+  const int64_t sb = B > 1 ? x.sb : std::max<int64_t>(x.sb, 8);
+  cuuint64_t strides[3] = {(cuuint64_t)sn * 2, (cuuint64_t)sh * 2, (cuuint64_t)sb * 2};
   cuuint32_t box[4] = {64, 128, 1, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x.ptr), dims, strides, box, es,
@@ -266,16 +301,19 @@ cs_status run_assign(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in k, int
                      int32_t* offs_k, const AssignScratch& sc, __nv_bfloat16* qp_out,
                      __nv_bfloat16* kp_out, cudaStream_t st, bool kmeans = false) {
   const int BH = B * H;
+  Nvtx range("cs.cocluster");
   const XView xq = view(q, H), xk = view(k, H);
   CS_CUDA(launch_init_sample(xq, xk, BH, N, d, kq, kk, seed, h_off, h_tot, init_q, init_k, cq, ck, st), "init_sample");
   for (int it = 0; it < iters; ++it) {
     const bool last = it == iters - 1;
     // Step A: query-aware key-side partitioning; k-means baseline: keys alone
+    Nvtx ra("cs.cocluster.step_a");
     if (kmeans) CS_CHECK(run_kmeans_step(B, H, N, d, k, kk, ck, lk, sc, st));
     else CS_CHECK(run_assign_step(B, H, N, d, k, kq, cq, kk, ck, lk, sc, st));
     CS_CUDA(launch_csort(lk, BH, N, kk, perm_k, offs_k, sc.hist, st), "csort_k");
     CS_CUDA(launch_seg_mean(xk, BH, N, d, kk, perm_k, offs_k, ck, last ? kp_out : nullptr, st), "seg_mean_k");
     // Step B: key-aware query-side partitioning; k-means baseline: queries alone
+    Nvtx rb("cs.cocluster.step_b");
     if (kmeans) CS_CHECK(run_kmeans_step(B, H, N, d, q, kq, cq, lq, sc, st));
     else CS_CHECK(run_assign_step(B, H, N, d, q, kk, ck, kq, cq, lq, sc, st));
     CS_CUDA(launch_csort(lq, BH, N, kq, perm_q, offs_q, sc.hist, st), "csort_q");
@@ -289,6 +327,7 @@ cs_status run_attn(int B, int H, int N, int d, int kq, int kk, const int32_t* pe
                    cs_bf16_out o, const AttnScratch& sc, cudaStream_t st, void* const* ev = nullptr,
                    const cs_peer_out* po = nullptr) {
   const int BH = B * H;
+  Nvtx range("cs.attention");
   CS_CUDA(launch_worklist(BH, kq, offs_q, sc.item_start, st), "worklist");
   CUtensorMap tq;
   KVMaps kv;
@@ -298,22 +337,12 @@ cs_status run_attn(int B, int H, int N, int d, int kq, int kk, const int32_t* pe
     CS_CHECK(make_map_2d(&kv.v[i], sc.vp, (uint64_t)BH * N, d, 8u << i));
   }
   if (ev) CS_CUDA(record_stage_event(ev[2], st), "event");
-  // opt-in persistent attention kernel (attn_persist.cu; measured neutral on Wan14B / Wan1.3B)
-  const bool persist = getenv("CS_ATTN_PERSIST") != nullptr;
-  if (persist)
-    CS_CUDA(launch_bsa_fwd_persist(&tq, &kv, BH, H, N, d, kq, kk, perm_q, offs_q, offs_k, n_keep, n_rows, kept,
-                                   sc.item_start, worklist_upper_bound(N, kq), scale,
-                                   static_cast<__nv_bfloat16*>(o.ptr), o.sb, po ? po->s_head : o.sh,
-                                   po ? po->s_tok : o.sn, po ? static_cast<const uint64_t*>(po->ptrs) : nullptr,
-                                   po ? po->n_per_rank : 0, po ? po->head_base : 0, st),
-            "bsa_fwd_persist");
-  else
-    CS_CUDA(launch_bsa_fwd(&tq, &kv, BH, H, N, d, kq, kk, perm_q, offs_q, offs_k, n_keep, n_rows, kept,
-                           sc.item_start, worklist_upper_bound(N, kq), scale,
-                           static_cast<__nv_bfloat16*>(o.ptr), o.sb, po ? po->s_head : o.sh,
-                           po ? po->s_tok : o.sn, po ? static_cast<const uint64_t*>(po->ptrs) : nullptr,
-                           po ? po->n_per_rank : 0, po ? po->head_base : 0, st),
-            "bsa_fwd");
+  CS_CUDA(launch_bsa_fwd(&tq, &kv, BH, H, N, d, kq, kk, perm_q, offs_q, offs_k, n_keep, n_rows, kept,
+                         sc.item_start, worklist_upper_bound(N, kq), scale,
+                         static_cast<__nv_bfloat16*>(o.ptr), o.sb, po ? po->s_head : o.sh,
+                         po ? po->s_tok : o.sn, po ? static_cast<const uint64_t*>(po->ptrs) : nullptr,
+                         po ? po->n_per_rank : 0, po ? po->head_base : 0, st),
+          "bsa_fwd");
   if (ev) CS_CUDA(record_stage_event(ev[3], st), "event");
   return CS_OK;
 }
@@ -366,8 +395,8 @@ static cs_status assign_entry(bool kmeans, int B, int H, int N, int d, cs_bf16_i
   CS_CHECK(check_k(kk, N, "kk"));
   if (iters < 1) return fail(CS_ERR_ARG, "iters must be >= 1 (got %d)", iters);
   CS_CHECK(check_heads(H, head_offset, heads_total));
-  CS_CHECK(check_bf16(q.ptr, q.sb, q.sh, q.sn, "q"));
-  CS_CHECK(check_bf16(k.ptr, k.sb, k.sh, k.sn, "k"));
+  CS_CHECK(check_t(q, B, H, N, d, "q"));
+  CS_CHECK(check_t(k, B, H, N, d, "k"));
   NEED(cq, "cq"); NEED(ck, "ck"); NEED(lq, "lq"); NEED(lk, "lk");
   NEED(perm_q, "perm_q"); NEED(offs_q, "offs_q"); NEED(perm_k, "perm_k"); NEED(offs_k, "offs_k");
   const int BH = B * H;
@@ -399,7 +428,7 @@ cs_status kmeans_assign_step(int B, int H, int N, int d, cs_bf16_in x, int ks, c
   g_err[0] = 0;
   CS_CHECK(check_dims(B, H, N, d));
   if (ks < 1 || ks > kMaxClusters) return fail(CS_ERR_ARG, "ks must be in [1, %d] (got %d)", kMaxClusters, ks);
-  CS_CHECK(check_bf16(x.ptr, x.sb, x.sh, x.sn, "x"));
+  CS_CHECK(check_t(x, B, H, N, d, "x"));
   NEED(c_self, "c_self"); NEED(labels, "labels");
   const int BH = B * H;
   CS_CHECK(check_ws(ws, ws_bytes, need_assign(BH, N, d, ks, ks)));
@@ -414,7 +443,7 @@ cs_status coclust_assign_step(int B, int H, int N, int d, cs_bf16_in x, int ka, 
   CS_CHECK(check_dims(B, H, N, d));
   if (ka < 1 || ka > kMaxClusters) return fail(CS_ERR_ARG, "ka must be in [1, %d] (got %d)", kMaxClusters, ka);
   if (ks < 1 || ks > kMaxClusters) return fail(CS_ERR_ARG, "ks must be in [1, %d] (got %d)", kMaxClusters, ks);
-  CS_CHECK(check_bf16(x.ptr, x.sb, x.sh, x.sn, "x"));
+  CS_CHECK(check_t(x, B, H, N, d, "x"));
   NEED(c_anchor, "c_anchor"); NEED(c_self, "c_self"); NEED(labels, "labels");
   const int BH = B * H;
   CS_CHECK(check_ws(ws, ws_bytes, need_assign(BH, N, d, ka, ks)));
@@ -428,7 +457,7 @@ cs_status coclust_update_centroids(int B, int H, int N, int d, cs_bf16_in x, int
   g_err[0] = 0;
   CS_CHECK(check_dims(B, H, N, d));
   CS_CHECK(check_k(k, N, "k"));
-  CS_CHECK(check_bf16(x.ptr, x.sb, x.sh, x.sn, "x"));
+  CS_CHECK(check_t(x, B, H, N, d, "x"));
   NEED(perm, "perm"); NEED(offs, "offs"); NEED(c_inout, "c_inout");
   if (x_perm && reinterpret_cast<uintptr_t>(x_perm) % 16) return fail(CS_ERR_ALIGN, "x_perm not 16-byte aligned");
   CS_CUDA(launch_seg_mean(view(x, H), B * H, N, d, k, perm, offs, c_inout, static_cast<__nv_bfloat16*>(x_perm),
@@ -495,10 +524,10 @@ cs_status block_sparse_attn_ex(int B, int H, int N, int d, cs_bf16_in q, cs_bf16
   CS_CHECK(check_dims(B, H, N, d));
   CS_CHECK(check_k(kq, N, "kq"));
   CS_CHECK(check_k(kk, N, "kk"));
-  CS_CHECK(check_bf16(q.ptr, q.sb, q.sh, q.sn, "q"));
-  CS_CHECK(check_bf16(k.ptr, k.sb, k.sh, k.sn, "k"));
-  CS_CHECK(check_bf16(v.ptr, v.sb, v.sh, v.sn, "v"));
-  CS_CHECK(check_bf16(o.ptr, o.sb, o.sh, o.sn, "o"));
+  CS_CHECK(check_t(q, B, H, N, d, "q"));
+  CS_CHECK(check_t(k, B, H, N, d, "k"));
+  CS_CHECK(check_t(v, B, H, N, d, "v"));
+  CS_CHECK(check_t(o, B, H, N, d, "o"));
   if (!(scale > 0.f)) return fail(CS_ERR_ARG, "scale must be > 0 (got %g)", (double)scale);
   NEED(perm_q, "perm_q"); NEED(offs_q, "offs_q"); NEED(perm_k, "perm_k"); NEED(offs_k, "offs_k");
   NEED(n_keep, "n_keep"); NEED(kept, "kept");
@@ -538,10 +567,10 @@ cs_status check_layer_args(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in 
     return fail(CS_ERR_ARG, "unknown flags 0x%x", sel_flags);
   if (!(scale > 0.f)) return fail(CS_ERR_ARG, "scale must be > 0 (got %g)", (double)scale);
   CS_CHECK(check_heads(H, head_offset, heads_total));
-  CS_CHECK(check_bf16(q.ptr, q.sb, q.sh, q.sn, "q"));
-  CS_CHECK(check_bf16(k.ptr, k.sb, k.sh, k.sn, "k"));
-  CS_CHECK(check_bf16(v.ptr, v.sb, v.sh, v.sn, "v"));
-  CS_CHECK(check_bf16(o.ptr, o.sb, o.sh, o.sn, "o"));
+  CS_CHECK(check_t(q, B, H, N, d, "q"));
+  CS_CHECK(check_t(k, B, H, N, d, "k"));
+  CS_CHECK(check_t(v, B, H, N, d, "v"));
+  CS_CHECK(check_t(o, B, H, N, d, "o"));
   NEED(budget, "budget");
   return CS_OK;
 }
@@ -560,6 +589,7 @@ cs_status run_layer(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in k, cs_b
                         s.ck, s.lq, s.lk, s.perm_q, s.offs_q, s.perm_k, s.offs_k, as, at.qp, at.kp, st,
                         (sel_flags & CS_CLUSTER_KMEANS) != 0));
     if (ev) CS_CUDA(record_stage_event(ev[0], st), "event");
+    Nvtx rs("cs.select");
     CS_CUDA(launch_block_select(BH, H, kq, kk, d, s.cq, s.ck, s.offs_q, s.offs_k, budget, tau, theta, rule,
                                 sel_flags & (CS_SEL_PER_ROW | CS_SEL_SIZE_WEIGHTED), s.n_keep, s.n_rows, s.kept,
                                 se.order, se.cnt, se.abar, st),
@@ -647,8 +677,8 @@ cs_status attention_density(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in
                             int passes, int32_t* counts, double* density, void* ws, size_t ws_bytes, void* stream) {
   g_err[0] = 0;
   CS_CHECK(check_dims(B, H, N, d));
-  CS_CHECK(check_bf16(q.ptr, q.sb, q.sh, q.sn, "q"));
-  CS_CHECK(check_bf16(k.ptr, k.sb, k.sh, k.sn, "k"));
+  CS_CHECK(check_t(q, B, H, N, d, "q"));
+  CS_CHECK(check_t(k, B, H, N, d, "k"));
   if (!(tau > 0.0 && tau <= 1.0)) return fail(CS_ERR_ARG, "tau must be in (0, 1] (got %g)", tau);
   if (!(scale > 0.f)) return fail(CS_ERR_ARG, "scale must be > 0 (got %g)", (double)scale);
   if (passes == 0) passes = 4;
@@ -706,14 +736,7 @@ typedef CUresult (*PtrAttrFn)(void*, CUpointer_attribute, CUdeviceptr);
 cs_status cs_ipc_handle(const void* dev_ptr, void* handle_out, size_t* offset_out) {
   g_err[0] = 0;
   NEED(dev_ptr, "dev_ptr"); NEED(handle_out, "handle_out"); NEED(offset_out, "offset_out");
-  static PtrAttrFn attr = nullptr;
-  if (!attr) {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuPointerGetAttribute", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      attr = reinterpret_cast<PtrAttrFn>(p);
-  }
+  PtrAttrFn attr = reinterpret_cast<PtrAttrFn>(driver_entry("cuPointerGetAttribute", g_attr_once, g_attr_fn));
   if (!attr) return fail(CS_ERR_CUDA, "cuPointerGetAttribute unavailable");
   CUdeviceptr base = 0;
   if (attr(&base, CU_POINTER_ATTRIBUTE_RANGE_START_ADDR, reinterpret_cast<CUdeviceptr>(dev_ptr)) != CUDA_SUCCESS)

@@ -301,6 +301,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     for (int t = 0; t < 2; ++t) { mbar_init(acc_full + t, 1); mbar_init(acc_empty + t, 8); }
     fence_barrier_init();
   }
+#ifdef CS_PAIR_PRESYNC
+  cluster_sync_all();  // racecheck experiment: both CTAs past their prologue before the collective alloc
+#endif
   if (warp == WARP_MMA) tmem_alloc_pair(tmem_slot, 512);
   tc_fence_before();
   cluster_sync_all();  // barriers initialised and TMEM allocated in both CTAs

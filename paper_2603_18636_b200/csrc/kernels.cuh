@@ -75,14 +75,6 @@ cudaError_t launch_bsa_fwd(const CUtensorMap* tm_q, const KVMaps* kv,
                            long long osn, const uint64_t* peer_ptrs, int peer_npr,
                            int peer_head_base, cudaStream_t st);
 
-// ---- attn_persist.cu : the same attention as a persistent kernel (one CTA per SM over the items)
-cudaError_t launch_bsa_fwd_persist(const CUtensorMap* tm_q, const KVMaps* kv, int BH, int H, int N, int d, int kq,
-                                   int kk, const int32_t* perm_q, const int32_t* offs_q, const int32_t* offs_k,
-                                   const int32_t* n_keep, const int32_t* n_rows, const int32_t* kept,
-                                   const int32_t* item_start, int items_ub, float scale, __nv_bfloat16* o,
-                                   long long osb, long long osh, long long osn, const uint64_t* peer_ptrs,
-                                   int peer_npr, int peer_head_base, cudaStream_t st);
-
 // ---- peer.cu : cross-process peer memory (CUDA IPC) and a device-side barrier over peer flags
 cudaError_t launch_peer_barrier(int P, int rank, const uint64_t* peer_flags, int epoch, cudaStream_t st);
 

@@ -152,3 +152,27 @@ def test_extension_entry_argument_errors(L):
     assert L.cs_ipc_open(None, 0, ctypes.byref(ctypes.c_void_p())) == 1
     assert L.cs_ipc_close(None, 0) == 1
     assert L.cs_density_workspace_bytes(1, 2, 1000) > 0 and L.cs_density_workspace_bytes(0, 2, 1000) == 0
+
+
+def test_broadcast_and_overlapping_strides_rejected(L):
+    """a stride-0 (expand()ed) dimension of extent > 1 or overlapping rows would make
+    the TMA maps and the pointer-arithmetic kernels read different rows: rejected (CS_ERR_SHAPE)
+    before any launch.  Extent-1 dimensions may carry any stride."""
+    ok = _bf16(sb=0, sh=256 * 128, sn=128)
+    call = lambda q, B=1, H=2: L.coclust_assign(B, H, 256, 128, q, ok, 16, 16, 2, 0, 0, 0, None, None, FAKE, FAKE,
+                                                FAKE, FAKE, FAKE, FAKE, FAKE, FAKE, FAKE, 1 << 40, None)
+    assert call(_bf16(sb=0, sh=0, sn=128)) == 2 and b"broadcast" in L.cs_last_error()     # H = 2 over sh = 0
+    assert call(_bf16(sb=0, sh=256 * 128, sn=128), B=2) == 2                               # B = 2 over sb = 0
+    assert call(_bf16(sb=0, sh=256 * 128, sn=64)) == 2                                     # rows overlap
+    o = __import__("paper_2603_18636_b200")._BF16Out(FAKE, 0, 0, 128)                       # H = 1: sh = 0 is fine
+    q1 = _bf16(sb=0, sh=0, sn=128)
+    st = L.block_sparse_attn(1, 1, 256, 128, q1, q1, q1, 16, 16, FAKE, FAKE, FAKE, FAKE, FAKE, FAKE,
+                             0.1, o, None, 1 << 40, None)
+    assert st == 5  # passes the stride checks, stops at the NULL workspace
+
+
+def test_misaligned_workspace_rejected(L):
+    q = _bf16(sb=0, sh=256 * 128, sn=128)
+    st = L.coclust_assign(1, 2, 256, 128, q, q, 16, 16, 2, 0, 0, 0, None, None, FAKE, FAKE, FAKE, FAKE, FAKE,
+                          FAKE, FAKE, FAKE, ctypes.c_void_p(0x10004), 1 << 40, None)
+    assert st == 4 and b"workspace" in L.cs_last_error()

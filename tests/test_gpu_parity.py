@@ -661,27 +661,6 @@ def test_batch_of_two_layers(pb, kk):
             assert err.max() <= ATOL_MAX and err.mean() <= ATOL_MEAN, (b, h, err.max())
 
 
-def test_persistent_attention_variant_matches(pb, monkeypatch):
-    """The opt-in persistent attention kernel (CS_ATTN_PERSIST, one CTA per SM over the work
-    items, double-buffered unit tables, cross-item Q / O hand-off) gives the same bits as the
-    default kernel (same tiles, same summation order), on pair and split-KV items and on several
-    items per CTA."""
-    w = video_qkv(6, 24, 40, 3, 128, seed=70)            # N = 5760: ~3 x 40 items on 148 CTAs
-    budget = torch.tensor([0.2, 0.35, 1.0], dtype=torch.float32).cuda()
-    q, k, v = w.q.cuda(), w.k.cuda(), w.v.cuda()
-    ref = pb.coclust_sparse_attention(q, k, v, 40, 120, 2, budget, seed=2)
-    monkeypatch.setenv("CS_ATTN_PERSIST", "1")
-    got = pb.coclust_sparse_attention(q, k, v, 40, 120, 2, budget, seed=2)
-    big = video_qkv(21, 45, 80, 2, 128, seed=71, device="cuda")  # ~700 items: ~5 per CTA
-    b2 = torch.tensor([0.2, 0.3], dtype=torch.float32).cuda()
-    got2 = pb.coclust_sparse_attention(big.q, big.k, big.v, 100, 500, 2, b2)
-    monkeypatch.delenv("CS_ATTN_PERSIST")
-    ref2 = pb.coclust_sparse_attention(big.q, big.k, big.v, 100, 500, 2, b2)
-    torch.cuda.synchronize()
-    assert torch.equal(got, ref)
-    assert torch.equal(got2, ref2)
-
-
 def test_attn_many_small_clusters_1024(pb):
     """K_q = K_k = 1024 (the ABI maximum) on N = 8192: query clusters of ~8 rows (every item a
     single-tile split-KV item), key clusters of ~8 keys (one 8-row unit each, heavy masking).
