@@ -56,6 +56,9 @@ def parse():
     ap.add_argument("--ulysses-return", choices=["fused", "nccl"], default="fused",
                     help="Ulysses output path: attention epilogue stores into the owners' token blocks "
                          "(fused, CUDA IPC / NVLink) or NCCL all_to_all + unpack")
+    ap.add_argument("--ulysses-overlap", choices=["on", "off"], default="off",
+                    help="Ulysses in-bound: packed Q|K exchange + V's exchange on a side stream overlapping the "
+                         "co-clustering (on), or one packed Q|K|V exchange (off)")
     ap.add_argument("--graph", choices=["on", "off"], default="on",
                     help="time the layer as CUDA-graph replays (one captured layer call; head-parallel)")
     return ap.parse_args()
@@ -179,7 +182,7 @@ def bench_config(args, H, N, d, world, mode, tensor_bytes):
     return {"workload": CONFIG_NAMES[args.config], "B": 1, "H": H, "N": N, "d": d,
             "kq": args.kq, "kk": args.kk, "iters": args.iters, "budget": args.budget,
             "rule": args.rule, "tau": args.tau, "theta": args.theta, "sel_flags": args.sel_flags,
-            "parallelism": (f"ulysses-a2a x{world} (return: {args.ulysses_return})" if mode == "ulysses"
+            "parallelism": (f"ulysses-a2a x{world} (return: {args.ulysses_return}, V overlap: {args.ulysses_overlap})" if mode == "ulysses"
                             else f"head-parallel x{world}"),
             "l2": "inputs larger than L2 (%.0f MB/tensor/rank)" % (tensor_bytes / 1e6)}
 
@@ -255,7 +258,8 @@ def run_ours(args):
         tok = lambda t: t[0].permute(1, 0, 2)[rank * Nl:(rank + 1) * Nl].unsqueeze(0).contiguous()
         q, k, v = tok(full.q), tok(full.k), tok(full.v)          # [1, N/P, H, d] token blocks
         q_h, k_h = full.q[:, h0:h1].contiguous(), full.k[:, h0:h1].contiguous()  # for F_kept only
-        kw = dict(seed=args.seed, tau=args.tau, theta=args.theta, rule=rule, ws=ws)
+        kw = dict(seed=args.seed, tau=args.tau, theta=args.theta, rule=rule, ws=ws,
+                  overlap_v=args.ulysses_overlap == "on")
         if args.ulysses_return == "fused":
             from paper_2603_18636_b200.dist import PeerOutput, ulysses_layer_fused
             peer = PeerOutput(Nl, H_total, d, dev)

@@ -281,6 +281,29 @@ cs_status coclust_sparse_attention_peer(int H, int N, int d, cs_bf16_in q, cs_bf
                                         const cs_peer_out* o, void* ws, size_t ws_bytes,
                                         void* stream, void* const* stage_events);
 
+/* The Ulysses layer entry (B = 1): coclust_sparse_attention_ex on the [1, H, N, d]
+ * strided views of the in-bound all-to-all buffers, with two multi-GPU hooks:
+ *   v_ready  (nullable cudaEvent_t) — `stream` waits on it just before V is first read, after
+ *            co-clustering and selection (which read only Q and K): the caller's all-to-all of V
+ *            on another stream overlaps the whole clustering stage;
+ *   peer     (nullable) — output rows go to the owners' token blocks as in
+ *            coclust_sparse_attention_peer; o is ignored then.  Otherwise o receives the output. */
+cs_status coclust_sparse_attention_ulysses(int H, int N, int d, cs_bf16_in q, cs_bf16_in k,
+                                           cs_bf16_in v, int kq, int kk, int iters, uint64_t seed,
+                                           int head_offset, int heads_total, const float* budget,
+                                           double tau, double theta, int rule, int flags, float scale,
+                                           cs_bf16_out o, const cs_peer_out* peer, void* v_ready,
+                                           void* ws, size_t ws_bytes, void* stream,
+                                           void* const* stage_events);
+
+/* Ulysses in-bound pack (a13): T (1..4) rank-local token blocks srcs[t] = [Nl, P*Hl, d] bf16
+ * (host array of T device pointers, 16-byte aligned) -> dst [P, Nl, T, Hl, d]: chunk p holds the
+ * heads of rank p, and per token the T tensors' head rows side by side.  After one
+ * all_to_all_single of dst the receiver holds [N = P*Nl, T, Hl, d], in which tensor t is the
+ * [1, Hl, N, d] view with element strides (sh, sn) = (d, T*Hl*d) — passed to the layer as is. */
+cs_status cs_ulysses_pack(int Nl, int P, int Hl, int d, int T, const void* const* srcs, void* dst,
+                          void* stream);
+
 /* Device-side barrier over P ranks: peer_flags = DEVICE array of P uint64 pointers to every
  * rank's int32 flag array [P] (zero-initialised, mapped here); rank `rank` writes `epoch` into
  * flags_p[rank] of every rank p (system-scope release) after all earlier work on `stream`, then

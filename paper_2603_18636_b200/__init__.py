@@ -77,6 +77,10 @@ _SIG = {
                                            _I, _P, ctypes.c_double, ctypes.c_double, _I, _I, ctypes.c_float, _P, _P,
                                            ctypes.c_size_t, _P, _P]),
     "cs_peer_barrier": (_I, [_I, _I, _P, _I, _P]),
+    "coclust_sparse_attention_ulysses": (_I, [_I, _I, _I, _BF16In, _BF16In, _BF16In, _I, _I, _I, ctypes.c_uint64,
+                                              _I, _I, _P, ctypes.c_double, ctypes.c_double, _I, _I, ctypes.c_float,
+                                              _BF16Out, _P, _P, _P, ctypes.c_size_t, _P, _P]),
+    "cs_ulysses_pack": (_I, [_I, _I, _I, _I, _I, _P, _P, _P]),
     "cs_ipc_handle": (_I, [_P, _P, ctypes.POINTER(ctypes.c_size_t)]),
     "cs_ipc_open": (_I, [_P, ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)]),
     "cs_ipc_close": (_I, [_P, ctypes.c_size_t]),
@@ -99,6 +103,8 @@ def lib() -> ctypes.CDLL:
             raise ImportError(f"{LIB_PATH} not built; run `python -m paper_2603_18636_b200.build`")
         L = ctypes.CDLL(LIB_PATH)
         for name, (res, args) in _SIG.items():
+            if not hasattr(L, name):  # an older library build (A/B runs); tests check the full export list
+                continue
             f = getattr(L, name)
             f.restype = res
             f.argtypes = args
@@ -347,6 +353,58 @@ def coclust_sparse_attention_peer(q, k, v, kq, kk, iters, budget, *, peer_ptrs, 
                                                head_offset, heads_total, _ptr(budget), float(tau), float(theta),
                                                int(rule), int(flags), float(scale), ctypes.byref(po), w, wn,
                                                _stream(q), evs))
+
+
+def coclust_sparse_attention_ulysses(q, k, v, kq, kk, iters, budget, *, out=None, peer=None, v_ready=None,
+                                     seed=0, tau=0.95, theta=0.1, rule=RULE_DENSITY, flags=0, scale=None, ws=None,
+                                     head_offset=0, heads_total=0, stage_events=None):
+    """The Ulysses layer entry (B = 1): q/k/v are [1, H, N, d] strided views of the in-bound
+    all-to-all buffers.  v_ready: torch.cuda.Event the layer's stream waits on before V is first
+    read (V's all-to-all overlaps the co-clustering); peer: dict(ptrs, P, n_per_rank, head_base,
+    s_tok, s_head) for the fused return path (else the output goes to `out`)."""
+    _cuda(q, "q")
+    B, H, N, d = q.shape
+    if B != 1:
+        raise ValueError("the Ulysses layer entry needs B == 1")
+    scale = d ** -0.5 if scale is None else scale
+    po = None
+    if peer is not None:
+        po = _PeerOut(peer["ptrs"].data_ptr(), peer["P"], peer["n_per_rank"], peer["head_base"], peer["s_tok"],
+                      peer["s_head"])
+        o = _BF16Out(None, 0, 0, 0)
+    else:
+        out = torch.empty(B, H, N, d, dtype=torch.bfloat16, device=q.device) if out is None else out
+        o = _bf16(out, True)
+    w, wn = _ws(ws, workspace_bytes(B, H, N, d, kq, kk), q.device)
+    evs = None
+    if stage_events is not None:
+        evs = (ctypes.c_void_p * 4)(*[ctypes.c_void_p(e.cuda_event) for e in stage_events])
+    _check(lib().coclust_sparse_attention_ulysses(H, N, d, _bf16(q), _bf16(k), _bf16(v), kq, kk, iters, seed,
+                                                  head_offset, heads_total, _ptr(budget), float(tau), float(theta),
+                                                  int(rule), int(flags), float(scale), o,
+                                                  ctypes.byref(po) if po is not None else None,
+                                                  ctypes.c_void_p(v_ready.cuda_event) if v_ready is not None else None,
+                                                  w, wn, _stream(q), evs))
+    return out
+
+
+def ulysses_pack(blocks, P, out=None):
+    """T rank-local token blocks [1, Nl, P*Hl, d] (bf16, contiguous) -> [P, Nl, T, Hl, d] (one send
+    buffer for a single all_to_all_single of all T tensors)."""
+    x0 = blocks[0]
+    _cuda(x0, "blocks[0]")
+    _, Nl, H, d = x0.shape
+    T = len(blocks)
+    if H % P:
+        raise ValueError("H must be divisible by P")
+    Hl = H // P
+    for b in blocks:
+        if b.shape != x0.shape or not b.is_contiguous() or b.dtype != torch.bfloat16:
+            raise ValueError("blocks must be contiguous bf16 tensors of one shape")
+    out = torch.empty(P, Nl, T, Hl, d, dtype=torch.bfloat16, device=x0.device) if out is None else out
+    srcs = (ctypes.c_void_p * T)(*[b.data_ptr() for b in blocks])
+    _check(lib().cs_ulysses_pack(Nl, P, Hl, d, T, srcs, _ptr(out), _stream(x0)))
+    return out
 
 
 def peer_barrier(P, rank, flag_ptrs, epoch, stream_of):

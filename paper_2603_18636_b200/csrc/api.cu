@@ -579,7 +579,8 @@ cs_status check_layer_args(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in 
 cs_status run_layer(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in k, cs_bf16_in v, int kq, int kk,
                     int iters, uint64_t seed, int head_offset, int heads_total, const float* budget, double tau,
                     double theta, int rule, int sel_flags, float scale, cs_bf16_out o, const LayerState& s, bool recompute,
-                    Carve& c, cudaStream_t st, void* const* ev, const cs_peer_out* po = nullptr) {
+                    Carve& c, cudaStream_t st, void* const* ev, const cs_peer_out* po = nullptr,
+                    void* v_ready = nullptr) {
   const int BH = B * H;
   AttnScratch at = carve_attn(c, BH, N, d, kq);
   AssignScratch as = carve_assign(c, BH, N, d, kq, kk);
@@ -602,6 +603,9 @@ cs_status run_layer(int B, int H, int N, int d, cs_bf16_in q, cs_bf16_in k, cs_b
     CS_CUDA(launch_permute_rows(view(k, H), BH, N, d, s.perm_k, at.kp, st), "permute_k");
     if (ev) CS_CUDA(record_stage_event(ev[1], st), "event");
   }
+  // V is first read here: a caller still delivering it on another stream (the Ulysses in-bound
+  // all-to-all of V overlapping the co-clustering, which reads only Q and K) passes its event
+  if (v_ready) CS_CUDA(cudaStreamWaitEvent(st, static_cast<cudaEvent_t>(v_ready), 0), "wait v_ready");
   CS_CUDA(launch_permute_rows(view(v, H), BH, N, d, s.perm_k, at.vp, st), "permute_v");
   return run_attn(B, H, N, d, kq, kk, s.perm_q, s.offs_q, s.offs_k, s.n_keep, s.n_rows, s.kept, scale, o, at, st,
                   ev, po);
@@ -718,6 +722,47 @@ cs_status coclust_sparse_attention_peer(int H, int N, int d, cs_bf16_in q, cs_bf
   LayerState s = carve_state(c, H, N, d, kq, kk);
   return run_layer(1, H, N, d, q, k, v, kq, kk, iters, seed, head_offset, heads_total, budget, tau, theta, rule,
                    flags, scale, dummy, s, true, c, static_cast<cudaStream_t>(stream), stage_events, o);
+}
+
+cs_status coclust_sparse_attention_ulysses(int H, int N, int d, cs_bf16_in q, cs_bf16_in k, cs_bf16_in v, int kq,
+                                           int kk, int iters, uint64_t seed, int head_offset, int heads_total,
+                                           const float* budget, double tau, double theta, int rule, int flags,
+                                           float scale, cs_bf16_out o, const cs_peer_out* peer, void* v_ready,
+                                           void* ws, size_t ws_bytes, void* stream, void* const* stage_events) {
+  g_err[0] = 0;
+  cs_bf16_out out = o;
+  if (peer) {
+    NEED(peer->ptrs, "peer->ptrs");
+    if (peer->P < 1 || peer->n_per_rank < 1 || (long long)peer->P * peer->n_per_rank != N)
+      return fail(CS_ERR_SHAPE, "peer output: P * n_per_rank must equal N (%d * %d vs %d)", peer->P,
+                  peer->n_per_rank, N);
+    if (peer->head_base < 0 || peer->s_tok <= 0 || peer->s_head <= 0 || peer->s_tok % 8 || peer->s_head % 8)
+      return fail(CS_ERR_ALIGN, "peer output: strides must be positive multiples of 8 elements");
+    out = cs_bf16_out{const_cast<void*>(peer->ptrs), 0, peer->s_head, peer->s_tok};  // validated, never stored to
+  }
+  CS_CHECK(check_layer_args(1, H, N, d, q, k, v, kq, kk, iters, head_offset, heads_total, budget, tau, theta,
+                            rule, flags, scale, out));
+  CS_CHECK(check_ws(ws, ws_bytes, need_layer(H, N, d, kq, kk)));
+  Carve c(ws);
+  LayerState s = carve_state(c, H, N, d, kq, kk);
+  return run_layer(1, H, N, d, q, k, v, kq, kk, iters, seed, head_offset, heads_total, budget, tau, theta, rule,
+                   flags, scale, out, s, true, c, static_cast<cudaStream_t>(stream), stage_events, peer, v_ready);
+}
+
+cs_status cs_ulysses_pack(int Nl, int P, int Hl, int d, int T, const void* const* srcs, void* dst, void* stream) {
+  g_err[0] = 0;
+  if (Nl <= 0 || P <= 0 || Hl <= 0 || (d != 64 && d != 128)) return fail(CS_ERR_SHAPE, "Nl, P, Hl > 0, d in {64, 128}");
+  if (T < 1 || T > 4) return fail(CS_ERR_ARG, "T must be in [1, 4] (got %d)", T);
+  NEED(srcs, "srcs"); NEED(dst, "dst");
+  UlyssesSrcs u{};
+  for (int t = 0; t < T; ++t) {
+    NEED(srcs[t], "srcs[t]");
+    if (reinterpret_cast<uintptr_t>(srcs[t]) % 16) return fail(CS_ERR_ALIGN, "srcs[%d] not 16-byte aligned", t);
+    u.p[t] = static_cast<const uint4*>(srcs[t]);
+  }
+  if (reinterpret_cast<uintptr_t>(dst) % 16) return fail(CS_ERR_ALIGN, "dst not 16-byte aligned");
+  CS_CUDA(launch_ulysses_pack(Nl, P, T, (size_t)Hl * d * 2, u, dst, static_cast<cudaStream_t>(stream)), "ulysses_pack");
+  return CS_OK;
 }
 
 cs_status cs_peer_barrier(int P, int rank, const void* peer_flags, int epoch, void* stream) {

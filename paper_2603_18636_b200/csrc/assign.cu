@@ -301,9 +301,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     for (int t = 0; t < 2; ++t) { mbar_init(acc_full + t, 1); mbar_init(acc_empty + t, 8); }
     fence_barrier_init();
   }
-#ifdef CS_PAIR_PRESYNC
-  cluster_sync_all();  // racecheck experiment: both CTAs past their prologue before the collective alloc
-#endif
+  // Both CTAs past their prologue before the collective CTA-pair alloc: without this barrier
+  // compute-sanitizer racecheck reports the peer's half of tcgen05.alloc.cta_group::2 writing
+  // the slot while this CTA's alloc accesses it (scripts/micro/pair_alloc_race.cu: variants 2/3
+  // report it, variant 4 = this barrier does not; once per persistent CTA).
+  cluster_sync_all();
   if (warp == WARP_MMA) tmem_alloc_pair(tmem_slot, 512);
   tc_fence_before();
   cluster_sync_all();  // barriers initialised and TMEM allocated in both CTAs

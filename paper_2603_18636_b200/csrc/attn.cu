@@ -55,11 +55,6 @@ __device__ __forceinline__ int smid() {
 
 constexpr int BM = 128, BN = 128, UNIT = 8, UPT = BN / UNIT, NST = 2;
 constexpr int NTHREADS = 352;
-#ifdef CS_ATTN_NREG
-#define CS_ATTN_BOUNDS __maxnreg__(CS_ATTN_NREG)
-#else
-#define CS_ATTN_BOUNDS __launch_bounds__(NTHREADS, 1)
-#endif
 constexpr int WARP_PRODUCER = 8, WARP_MMA = 9, WARP_VLOAD = 10;
 constexpr float kRescaleThresh = 8.0f;
 #ifndef CS_POLY_EVERY
@@ -78,9 +73,8 @@ struct Smem {
   static constexpr int OFF_K = OFF_Q + 2 * QT;
   static constexpr int OFF_V = OFF_K + NST * KT;
   static constexpr int OFF_BAR = OFF_V + NST * KT;
-  // q_full, k_full[2], k_empty[2], v_full[2], v_empty[2], s_full[2], p_full[2 tiles][2 halves], o_full,
-  // pva_done[2]
-  static constexpr int OFF_MISC = OFF_BAR + 24 * 8;  // tmem slot, U, n
+  // q_full, k_full[2], k_empty[2], v_full[2], v_empty[2], s_full[2], p_full[2 tiles][2 halves], o_full
+  static constexpr int OFF_MISC = OFF_BAR + 16 * 8;  // tmem slot, U, n
   static constexpr int OFF_UROW = OFF_MISC + 16;      // [NST][UPT] unit start rows
   static constexpr int OFF_KSTART = OFF_UROW + NST * UPT * 4;
   static constexpr int OFF_KLEN = OFF_KSTART + kMaxClusters * 4;
@@ -91,7 +85,7 @@ struct Smem {
 };
 
 template <int D>
-__global__ void CS_ATTN_BOUNDS
+__global__ void __launch_bounds__(NTHREADS, 1)
     k_bsa_fwd(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ KVMaps kv, int H, int N,
               int kq, int kk, const int32_t* __restrict__ perm_q, const int32_t* __restrict__ offs_q,
               const int32_t* __restrict__ offs_k, const int32_t* __restrict__ n_keep,
@@ -112,7 +106,6 @@ __global__ void CS_ATTN_BOUNDS
   uint64_t* s_full = bars + 9;
   uint64_t* p_full = bars + 11;  // [tq * 2 + half]: P columns of keys [64 half, 64 half + 64)
   uint64_t* o_full = bars + 15;
-  uint64_t* pva_done = bars + 16;  // [tq]: PV(j) over the first 64 keys of tile j has completed
   int* misc = reinterpret_cast<int*>(sm + L::OFF_MISC);
   int* kstart = reinterpret_cast<int*>(sm + L::OFF_KSTART);
   int* klen = reinterpret_cast<int*>(sm + L::OFF_KLEN);
@@ -153,7 +146,6 @@ __global__ void CS_ATTN_BOUNDS
       for (int t = 0; t < 2; ++t) mbar_init(s_full + t, 1);
       for (int t = 0; t < 4; ++t) mbar_init(p_full + t, 128);
       mbar_init(o_full, 1);
-      for (int t = 0; t < 2; ++t) mbar_init(pva_done + t, 1);
       fence_barrier_init();
       tma_prefetch_desc(&tm_q);
       const int ntq = has1 ? 2 : 1;
@@ -313,9 +305,6 @@ __global__ void CS_ATTN_BOUNDS
       mbar_wait(p_full + tq * 2 + 0, j & 1);
       tc_fence_after();
       issue_pv(tq, slot, 0, j > 0);
-#ifdef CS_ATTN_SPLITMAX
-      commit(pva_done + tq);  // the softmax waits on it only to rescale O mid-tile (rare)
-#endif
       mbar_wait(p_full + tq * 2 + 1, j & 1);
       tc_fence_after();
       issue_pv(tq, slot, 1, true);
@@ -480,104 +469,6 @@ __global__ void CS_ATTN_BOUNDS
   if (MWV) {                                                                         \
     _Pragma("unroll") for (int r2 = 0; r2 < 32; ++r2) if ((MWV >> r2) & 1u) su[W * 32 + r2] = 0xff800000u; \
   }
-#ifdef CS_ATTN_SPLITMAX
-        // Per 64-key half: the row max of half A (keys 0-63) is taken while half B is still
-        // loading from TMEM, and its exponentials start with the running max updated by half A
-        // only.  Half B then uses the same running max unless its own max exceeds it by more than
-        // the lazy-rescale threshold — then (rare) O already holds PV(j, half A) at the old scale:
-        // wait for that MMA (pva_done) and rescale O before half B is signalled.
-        uint32_t su[BN];
-        tmem_ld32(s_tm, su);
-        tmem_ld32(s_tm + 32, su + 32);
-        tmem_wait_ld();
-        tmem_ld32(s_tm + 64, su + 64);
-        tmem_ld32(s_tm + 96, su + 96);
-        CS_APPLY_MASK(0, mw0)
-        CS_APPLY_MASK(1, mw1)
-        CS_TRACE(16 + tq, j);
-        const float2 sl2 = make_float2(scale_log2, scale_log2);
-        auto half_max = [&](int c0) -> float {
-          float mx8[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) mx8[i] = fmaxf(__uint_as_float(su[c0 + i]), __uint_as_float(su[c0 + 8 + i]));
-#pragma unroll
-          for (int c = c0 + 16; c < c0 + BN / 2; c += 16)
-#pragma unroll
-            for (int i = 0; i < 8; ++i) mx8[i] = fmax3(mx8[i], __uint_as_float(su[c + i]), __uint_as_float(su[c + 8 + i]));
-          return fmax3(fmax3(mx8[0], mx8[1], mx8[2]), fmax3(mx8[3], mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])) *
-                 scale_log2;
-        };
-        auto rescale_o = [&](float a) {
-#pragma unroll 1
-          for (int c = 0; c < D / 16; ++c) {
-            uint32_t ov[16];
-            tmem_ld16(o_tm + c * 16, ov);
-            tmem_wait_ld();
-#pragma unroll
-            for (int i = 0; i < 16; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * a);
-            tmem_st16(o_tm + c * 16, ov);
-          }
-        };
-        auto exps_half = [&](int hf) -> float {
-          const float2 nm2 = make_float2(-m, -m);
-          float2 acc4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-#pragma unroll
-          for (int c = hf * (BN / 2); c < (hf + 1) * (BN / 2); c += 2) {
-            const float2 x = ffma2(make_float2(__uint_as_float(su[c]), __uint_as_float(su[c + 1])), sl2, nm2);
-            const float2 p = (kPolyEvery > 0 && ((c >> 1) % kPolyEvery) == kPolyEvery - 1)
-                                 ? ex2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
-            acc4[(c >> 1) & 3] = fadd2(acc4[(c >> 1) & 3], p);
-            su[c >> 1] = pack_bf16x2(p.x, p.y);
-          }
-          const float2 s01 = fadd2(acc4[0], acc4[1]), s23 = fadd2(acc4[2], acc4[3]);
-          const float2 s4 = fadd2(s01, s23);
-          return s4.x + s4.y;
-        };
-        {
-          const float mxA = half_max(0);
-          CS_TRACE(12 + tq, j);
-          float alpha = 1.f;
-          if (j == 0) {
-            m = mxA;
-          } else if (mxA > m + kRescaleThresh) {
-            alpha = ex2(m - mxA);
-            l *= alpha;
-            m = mxA;
-          }
-          const bool warp_rescale = __any_sync(0xffffffffu, alpha != 1.f);
-          l += exps_half(0);
-          tmem_st32(s_tm, su);
-          // lazy O rescale before PV(j) starts (it waits for p_full(j, half 0)); O is stable:
-          // PV(j-1) completed before s_full(j) (same commit order)
-          if (warp_rescale) rescale_o(alpha);
-          tmem_wait_st();
-          tc_fence_before();
-          mbar_arrive(p_full + tq * 2 + 0);
-          CS_TRACE(14 + tq, j);
-        }
-        {
-          tmem_wait_ld();
-          CS_APPLY_MASK(2, mw2)
-          CS_APPLY_MASK(3, mw3)
-          const float mxB = half_max(BN / 2);
-          float alpha = 1.f;
-          if (mxB > m + kRescaleThresh) {
-            alpha = ex2(m - mxB);
-            l *= alpha;
-            m = mxB;
-          }
-          if (__any_sync(0xffffffffu, alpha != 1.f)) {
-            mbar_wait(pva_done + tq, j & 1);
-            tc_fence_after();
-            rescale_o(alpha);
-          }
-          l += exps_half(1);
-          tmem_st32(s_tm + 32, su + 32);
-          tmem_wait_st();
-          tc_fence_before();
-          mbar_arrive(p_full + tq * 2 + 1);
-        }
-#else
         uint32_t su[BN];
 #pragma unroll
         for (int c = 0; c < BN / 32; ++c) tmem_ld32(s_tm + c * 32, su + c * 32);
@@ -650,7 +541,6 @@ __global__ void CS_ATTN_BOUNDS
         const float2 s01 = fadd2(acc4[0], acc4[1]), s23 = fadd2(acc4[2], acc4[3]);
         const float2 s4 = fadd2(s01, s23);
         l += s4.x + s4.y;
-#endif
 #undef CS_APPLY_MASK
         CS_TRACE(6 + 2 * tq, j);
         if (j + 1 < my_nt) tile_mask(split ? 2 * (j + 1) + tq : j + 1);

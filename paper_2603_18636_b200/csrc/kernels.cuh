@@ -39,6 +39,11 @@ cudaError_t launch_seg_mean(XView x, int BH, int N, int d, int K, const int32_t*
 cudaError_t launch_csort(const int32_t* lab, int BH, int N, int K, int32_t* perm, int32_t* offs,
                          int32_t* hist, cudaStream_t st);
 cudaError_t launch_block_transpose(int A, int B, size_t row_bytes, const void* src, void* dst, cudaStream_t st);
+struct UlyssesSrcs {
+  const uint4* p[4];
+};
+cudaError_t launch_ulysses_pack(int Nl, int P, int T, size_t row_bytes, const UlyssesSrcs& srcs, void* dst,
+                                cudaStream_t st);
 cudaError_t launch_permute_rows(XView x, int BH, int N, int d, const int32_t* perm,
                                 __nv_bfloat16* xp, cudaStream_t st);
 

@@ -6,10 +6,11 @@ heads_total = H — the R4 sampler streams are keyed by the global head, so each
 bit-identical to a single-GPU run.  No collective on the data path.
 
 Ulysses (BASELINE configs[3]): each rank holds a token block [B=1, N/P, H, d] of Q, K,
-V.  One all_to_all_single per tensor (NCCL over NVLink) turns it into all N tokens of H/P heads;
-the layer runs on those heads (the ABI takes the [N, H/P, d] buffer through strides, no copy);
-one all_to_all_single brings O back to the token block.  The only data movement besides the
-collectives is the pack / unpack block transpose (cs_block_transpose, our kernel).
+V.  One all_to_all_single of the packed Q|K buffer (cs_ulysses_pack, our kernel) turns it into all
+N tokens of H/P heads; the layer reads them from the receive buffer through strides (no copy).
+V's all_to_all_single runs on a side stream while the layer co-clusters (Alg. 1 reads only Q and
+K); the layer waits on V's event just before its V permute.  O comes back with one
+all_to_all_single + unpack (cs_block_transpose) or, fused, through the attention epilogue.
 
 Fused return path (`ulysses_layer_fused`): the output token blocks of all ranks are mapped into
 every process (CUDA IPC; over NVLink on a multi-GPU box) and the attention epilogue stores each
@@ -42,29 +43,66 @@ def head_parallel_layer(q, k, v, kq, kk, iters, budget, *, rank: int, world: int
     return out, (lo, hi)
 
 
-def _cuda_transpose(x, A, B):
-    import paper_2603_18636_b200 as pb
-    return pb.block_transpose(x, A, B)
+class CudaOps:
+    """The device operations of the Ulysses layer (all of them libcoclust kernels): the in-bound
+    pack, the layer entry, the out-bound unpack, the device barrier, and the side stream V's
+    exchange runs on.  The CPU tests substitute a reference implementation of the same contract."""
+
+    def pack(self, blocks, P):
+        import paper_2603_18636_b200 as pb
+        return pb.ulysses_pack(blocks, P)
+
+    def transpose(self, x, A, B):
+        import paper_2603_18636_b200 as pb
+        return pb.block_transpose(x, A, B)
+
+    def layer(self, q, k, v, kq, kk, iters, budget, **kw):
+        import paper_2603_18636_b200 as pb
+        return pb.coclust_sparse_attention_ulysses(q, k, v, kq, kk, iters, budget, **kw)
+
+    def barrier(self, peer, P, r, like):
+        import paper_2603_18636_b200 as pb
+        pb.peer_barrier(P, r, peer.flag_ptrs, peer.epoch, like)
+
+    def exchange_async(self, send, a2a):
+        """a2a of `send` on a side stream ordered after the current stream; -> (recv, event)."""
+        import torch
+        cur = torch.cuda.current_stream(send.device)
+        side = torch.cuda.Stream(send.device)
+        side.wait_stream(cur)
+        with torch.cuda.stream(side):
+            recv = torch.empty_like(send)
+            a2a(recv, send)
+            ev = torch.cuda.Event()
+            ev.record(side)
+        recv.record_stream(cur)
+        send.record_stream(side)
+        return recv, ev
 
 
-def _cuda_layer(q, k, v, kq, kk, iters, budget, head_offset, heads_total, **kw):
-    import paper_2603_18636_b200 as pb
-    return pb.coclust_sparse_attention(q, k, v, kq, kk, iters, budget, head_offset=head_offset,
-                                       heads_total=heads_total, **kw)
-
-
-def ulysses_layer(q_loc, k_loc, v_loc, kq, kk, iters, budget, *, group=None, transpose=None,
-                  layer=None, **kw):
-    """Sequence-parallel SVOO layer.
+def ulysses_layer(q_loc, k_loc, v_loc, kq, kk, iters, budget, *, group=None, a2a=None, peer=None,
+                  overlap_v=False, ops=None, **kw):
+    """Sequence-parallel SVOO layer (SURVEY §8e, a13).
 
     q_loc, k_loc, v_loc: [1, N/P, H, d] bf16 token blocks of this rank (rank r holds tokens
     [r N/P, (r+1) N/P)); budget: [H] float32 for the whole layer.  Returns o_loc [1, N/P, H, d].
-    `transpose` / `layer` default to the CUDA library (overridable for CPU tests of the logic).
+
+    In-bound (default): ONE all_to_all_single of the packed Q|K|V send buffer (cs_ulysses_pack:
+    per destination rank, per token, the Q, K and V head rows side by side); the layer reads its
+    H/P heads straight from the receive buffer through strides.  overlap_v=True instead exchanges
+    Q|K first and V in a second all_to_all_single on a side stream, overlapped with the
+    co-clustering and selection (which read only Q and K): the layer's stream waits on V's event
+    just before the V permute (coclust_sparse_attention_ulysses, v_ready).  On one GPU (P = 1,
+    where the exchange is a local copy) that variant is erratic (occasional +10-14 ms layers) and
+    not faster, so it is opt-in; its value on an NVLink box is unmeasured.
+    Out-bound: `peer` (a PeerOutput) -> the attention epilogue stores every row straight into the
+    owning rank's token block (fused return, then a device barrier); else one all_to_all_single of
+    O + unpack.  `a2a(recv, send)` overrides the exchange (e.g. through host memory for a gloo
+    group); `ops` overrides the device operations (CudaOps).
     """
     import torch
     import torch.distributed as dist
-    transpose = transpose or _cuda_transpose
-    layer = layer or _cuda_layer
+    ops = ops or CudaOps()
     P = dist.get_world_size(group)
     r = dist.get_rank(group)
     B, Nl, H, d = q_loc.shape
@@ -72,24 +110,41 @@ def ulysses_layer(q_loc, k_loc, v_loc, kq, kk, iters, budget, *, group=None, tra
         raise ValueError("Ulysses path needs B == 1 and H divisible by the group size")
     Hl = H // P
     N = Nl * P
-    full = []
-    for x in (q_loc, k_loc, v_loc):
-        # pack: [Nl, P, Hl, d] -> [P, Nl, Hl, d] (chunk p = the heads of rank p)
-        send = transpose(x.contiguous().view(Nl, P * Hl * d), Nl, P)
-        recv = torch.empty_like(send)  # [P (source = token block), Nl, Hl, d] == [N, Hl, d]
-        dist.all_to_all_single(recv, send, group=group)
-        # [N, Hl, d] buffer seen as [B=1, Hl, N, d]: strides (N Hl d, d, Hl d)
-        full.append(recv.view(N, Hl, d).permute(1, 0, 2).unsqueeze(0))
+    a2a = a2a or (lambda recv, send: dist.all_to_all_single(recv, send, group=group))
+    blocks = [x.contiguous() for x in (q_loc, k_loc, v_loc)]
+    v_ready = None
+    if overlap_v:
+        send_qk = ops.pack(blocks[:2], P)                        # [P, Nl, 2, Hl, d]
+        recv_qk = torch.empty_like(send_qk)
+        a2a(recv_qk, send_qk)                                    # first: the clustering needs it
+        send_v = ops.pack(blocks[2:], P)                         # [P, Nl, 1, Hl, d]
+        recv_v, v_ready = ops.exchange_async(send_v, a2a)        # overlaps the co-clustering
+        T_qk, qk_buf = 2, recv_qk
+        v_view = recv_v.view(N, Hl, d).permute(1, 0, 2).unsqueeze(0)   # strides (.., d, Hl d, 1)
+    else:
+        send = ops.pack(blocks, P)                               # [P, Nl, 3, Hl, d]
+        recv = torch.empty_like(send)
+        a2a(recv, send)
+        T_qk, qk_buf = 3, recv
+        v_view = recv.view(N, 3, Hl, d)[:, 2].permute(1, 0, 2).unsqueeze(0)
+    # [N, T, Hl, d] receive buffer: tensor t is the [1, Hl, N, d] view with strides (d, T Hl d)
+    view = lambda t: qk_buf.view(N, T_qk, Hl, d)[:, t].permute(1, 0, 2).unsqueeze(0)
+    kw.setdefault("head_offset", r * Hl)
+    kw.setdefault("heads_total", H)
+    bud = budget[r * Hl:(r + 1) * Hl].contiguous()
+    if peer is not None:
+        ops.layer(view(0), view(1), v_view, kq, kk, iters, bud, v_ready=v_ready,
+                  peer=dict(ptrs=peer.ptrs, P=P, n_per_rank=Nl, head_base=r * Hl, s_tok=H * d, s_head=d), **kw)
+        peer.epoch += 1
+        ops.barrier(peer, P, r, q_loc)
+        return peer.out
     out_buf = torch.empty(N, Hl, d, dtype=q_loc.dtype, device=q_loc.device)
     o_view = out_buf.permute(1, 0, 2).unsqueeze(0)  # written in place through strides
-    res = layer(full[0], full[1], full[2], kq, kk, iters, budget[r * Hl:(r + 1) * Hl].contiguous(),
-                r * Hl, H, out=o_view, **kw)
-    if res is not None and res.data_ptr() != o_view.data_ptr():
-        o_view.copy_(res)
+    ops.layer(view(0), view(1), v_view, kq, kk, iters, bud, v_ready=v_ready, out=o_view, **kw)
     back = torch.empty_like(out_buf)  # [P (source = head block), Nl, Hl, d]
-    dist.all_to_all_single(back, out_buf.view(P, Nl * Hl * d), group=group)
+    a2a(back.view(P, Nl * Hl * d), out_buf.view(P, Nl * Hl * d))
     # unpack: [P, Nl, Hl, d] -> [Nl, P, Hl, d] = [Nl, H, d]
-    o_loc = transpose(back.view(P, Nl * Hl * d), P, Nl)
+    o_loc = ops.transpose(back.view(P, Nl * Hl * d), P, Nl)
     return o_loc.view(1, Nl, H, d)
 
 
@@ -137,30 +192,5 @@ class PeerOutput:
 def ulysses_layer_fused(q_loc, k_loc, v_loc, kq, kk, iters, budget, peer: "PeerOutput", *, group=None,
                         a2a=None, **kw):
     """ulysses_layer with the return all-to-all fused into the attention epilogue (see module doc).
-
-    Returns peer.out [1, N/P, H, d], complete once the calling stream passes the device barrier.
-    `a2a(recv, send)` overrides the input all_to_all_single (e.g. through host memory for a gloo
-    group in tests)."""
-    import torch
-    import torch.distributed as dist
-    import paper_2603_18636_b200 as pb
-    P = dist.get_world_size(group)
-    r = dist.get_rank(group)
-    B, Nl, H, d = q_loc.shape
-    if B != 1 or H % P:
-        raise ValueError("Ulysses path needs B == 1 and H divisible by the group size")
-    Hl = H // P
-    N = Nl * P
-    a2a = a2a or (lambda recv, send: dist.all_to_all_single(recv, send, group=group))
-    full = []
-    for x in (q_loc, k_loc, v_loc):
-        send = pb.block_transpose(x.contiguous().view(Nl, P * Hl * d), Nl, P)
-        recv = torch.empty_like(send)
-        a2a(recv, send)
-        full.append(recv.view(N, Hl, d).permute(1, 0, 2).unsqueeze(0))
-    pb.coclust_sparse_attention_peer(full[0], full[1], full[2], kq, kk, iters, budget[r * Hl:(r + 1) * Hl].contiguous(),
-                                     peer_ptrs=peer.ptrs, P=P, n_per_rank=Nl, head_base=r * Hl, s_tok=H * d,
-                                     s_head=d, head_offset=r * Hl, heads_total=H, **kw)
-    peer.epoch += 1
-    pb.peer_barrier(P, r, peer.flag_ptrs, peer.epoch, full[0])
-    return peer.out
+    Returns peer.out [1, N/P, H, d], complete once the calling stream passes the device barrier."""
+    return ulysses_layer(q_loc, k_loc, v_loc, kq, kk, iters, budget, group=group, a2a=a2a, peer=peer, **kw)

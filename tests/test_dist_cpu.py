@@ -78,23 +78,38 @@ def test_two_rank_head_parallel_matches_single_process():
         assert np.array_equal(got[h], ref.O)
 
 
-def _cpu_transpose(x, A, B):
-    return x.reshape(A, B, -1).transpose(0, 1).contiguous().reshape(B, -1)
+class _CpuOps:
+    """Reference implementation of the Ulysses device operations (paper_2603_18636_b200.dist.CudaOps)
+    with the same contracts, so the host logic (pack layout, strided views, head offsets, the two
+    exchanges, unpack) runs under gloo on CPU."""
+
+    def pack(self, blocks, P):  # cs_ulysses_pack: [1, Nl, P*Hl, d] x T -> [P, Nl, T, Hl, d]
+        _, Nl, H, d = blocks[0].shape
+        st = torch.stack([b[0].reshape(Nl, P, H // P, d) for b in blocks], dim=2)   # [Nl, P, T, Hl, d]
+        return st.permute(1, 0, 2, 3, 4).contiguous()
+
+    def transpose(self, x, A, B):  # cs_block_transpose
+        return x.reshape(A, B, -1).transpose(0, 1).contiguous().reshape(B, -1)
+
+    def layer(self, q, k, v, kq, kk, iters, budget, out=None, peer=None, v_ready=None, head_offset=0,
+              heads_total=0, **kw):
+        """The layer contract (global-head sampler streams) through the oracle."""
+        from oracle import svoo
+        f = lambda t: t.double().numpy()
+        for h in range(q.shape[1]):
+            r = svoo.coclust_sparse_attention_head(f(q[0, h]), f(k[0, h]), f(v[0, h]), kq, kk, iters, 3,
+                                                   float(budget[h]), 0.95, 0.1, svoo.RULE_DENSITY,
+                                                   h=head_offset + h, H=heads_total)
+            out[0, h].copy_(torch.from_numpy(r.O))
+        return out
+
+    def exchange_async(self, send, a2a):
+        recv = torch.empty_like(send)
+        a2a(recv, send)
+        return recv, None
 
 
-def _oracle_layer(q, k, v, kq, kk, iters, budget, head_offset, heads_total, out=None, **kw):
-    """CPU stand-in for the CUDA layer with the same contract (global-head sampler streams)."""
-    from oracle import svoo
-    f = lambda t: t.double().numpy()
-    for h in range(q.shape[1]):
-        r = svoo.coclust_sparse_attention_head(f(q[0, h]), f(k[0, h]), f(v[0, h]), kq, kk, iters, 3,
-                                               float(budget[h]), 0.95, 0.1, svoo.RULE_DENSITY,
-                                               h=head_offset + h, H=heads_total)
-        out[0, h].copy_(torch.from_numpy(r.O))
-    return out
-
-
-def _ulysses_worker(rank, world, port, ret):
+def _ulysses_worker(rank, world, port, overlap_v, ret):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2603_18636_b200.dist import ulysses_layer
@@ -104,8 +119,7 @@ def _ulysses_worker(rank, world, port, ret):
     Nl = N // world
     blk = lambda t: t[0].permute(1, 0, 2)[rank * Nl:(rank + 1) * Nl].unsqueeze(0).double().contiguous()
     budget = torch.tensor([0.3, 0.2, 0.5, 0.25])
-    o = ulysses_layer(blk(w.q), blk(w.k), blk(w.v), 6, 10, 2, budget, transpose=_cpu_transpose,
-                      layer=_oracle_layer)
+    o = ulysses_layer(blk(w.q), blk(w.k), blk(w.v), 6, 10, 2, budget, ops=_CpuOps(), overlap_v=overlap_v)
     gathered = [None] * world
     dist.all_gather_object(gathered, (rank, o.numpy()))
     if rank == 0:
@@ -114,16 +128,18 @@ def _ulysses_worker(rank, world, port, ret):
     dist.destroy_process_group()
 
 
-def test_two_rank_ulysses_matches_single_process():
-    """Sequence-sharded inputs -> all-to-all -> per-head layer -> all-to-all back == the layer
-    run on the whole sequence in one process (same per-head sampler streams)."""
+@pytest.mark.parametrize("overlap_v", [True, False])
+def test_two_rank_ulysses_matches_single_process(overlap_v):
+    """Sequence-sharded inputs -> packed Q|K all-to-all (+ V's own, or one packed Q|K|V) -> per-head
+    layer on the strided receive views -> all-to-all back + unpack == the layer run on the whole
+    sequence in one process (same per-head sampler streams)."""
     from oracle import svoo
     from synthetic import video_qkv
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_ulysses_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_ulysses_worker, args=(r, world, port, overlap_v, q)) for r in range(world)]
     for p in procs:
         p.start()
     got = q.get(timeout=300)          # [1, N, H, d]
@@ -137,3 +153,18 @@ def test_two_rank_ulysses_matches_single_process():
         ref = svoo.coclust_sparse_attention_head(f(w.q), f(w.k), f(w.v), 6, 10, 2, 3, budget[h], 0.95, 0.1,
                                                  svoo.RULE_DENSITY, h=h, H=4)
         np.testing.assert_allclose(got[0, :, h, :], ref.O, atol=1e-12)
+
+
+def test_ulysses_pack_layout_reference():
+    """The pack contract (include/coclust.h cs_ulysses_pack) on a labelled tensor: after the
+    exchange the receiver's [N, T, Hl, d] buffer holds tensor t, head p*Hl + hl of token n at
+    [n, t, hl] — checked by simulating the all-to-all of P ranks' packed buffers."""
+    P, Nl, Hl, d, T = 3, 4, 2, 8, 2
+    H, N = P * Hl, P * Nl
+    full = [torch.arange(N * H * d, dtype=torch.float64).reshape(1, N, H, d) + 1000 * t for t in range(T)]
+    ops = _CpuOps()
+    sends = [ops.pack([x[:, r * Nl:(r + 1) * Nl].contiguous() for x in full], P) for r in range(P)]
+    for dst in range(P):
+        recv = torch.cat([sends[src][dst] for src in range(P)])          # [N, T, Hl, d] (source-major)
+        for t in range(T):
+            assert torch.equal(recv[:, t], full[t][0, :, dst * Hl:(dst + 1) * Hl])
