@@ -50,13 +50,15 @@ __global__ void __launch_bounds__(256) k_init_sample(XView q, XView k, int N, in
                                                      float* __restrict__ cq, float* __restrict__ ck) {
   extern __shared__ uint32_t sm_bits[];
   __shared__ int sbuf[32];
+  // grid (BH, 2 sides, G): every CTA of a (bh, side) draws the same (deterministic) sample and
+  // gathers its own 1/G of the K centroid rows, so the gather is spread over many SMs
   const int bh = blockIdx.x, side = blockIdx.y;
   const int K = side ? kk : kq;
   const int32_t* init = side ? init_k : init_q;
   const XView X = side ? k : q;
   float* C = (side ? ck : cq) + (size_t)bh * K * d;
   const int nwords = (N + 31) >> 5;
-  int* idx = reinterpret_cast<int*>(sm_bits + nwords);
+  int* idx = reinterpret_cast<int*>(sm_bits + ((nwords + 3) & ~3));  // 16-byte aligned (int4 loads)
   if (init) {
     for (int j = threadIdx.x; j < K; j += blockDim.x) idx[j] = init[(size_t)bh * K + j];
   } else {
@@ -89,8 +91,14 @@ __global__ void __launch_bounds__(256) k_init_sample(XView q, XView k, int N, in
     for (int i = threadIdx.x; i < K; i += blockDim.x) {
       const int t = idx[i];
       if (t < NK) {
-        bool dup = false;
-        for (int k2 = 0; k2 < i && !dup; ++k2) dup = idx[k2] == t;
+        // branch-free scan of the earlier draws, 4 per broadcast 16-byte load (every lane of the
+        // warp reads the same addresses in the same iteration)
+        int dup = 0, k2 = 0;
+        for (; k2 + 4 <= i; k2 += 4) {
+          const int4 v = *reinterpret_cast<const int4*>(idx + k2);
+          dup |= (v.x == t) | (v.y == t) | (v.z == t) | (v.w == t);
+        }
+        for (; k2 < i; ++k2) dup |= idx[k2] == t;
         pick[i] = dup ? NK + i : t;
       } else if (t == NK + i) {
         pick[i] = t;
@@ -143,8 +151,10 @@ __global__ void __launch_bounds__(256) k_init_sample(XView q, XView k, int N, in
   // in flight per thread before the converts / stores (one launch per layer: latency matters)
   const int b = bh / X.H, h = bh % X.H;
   const int vpr = d / 8;  // 16-byte vectors per row
-  const int total = K * vpr;
-  for (int e0 = threadIdx.x; e0 < total; e0 += 4 * blockDim.x) {
+  const int per = (K + gridDim.z - 1) / gridDim.z;
+  const int jbeg = min(K, (int)blockIdx.z * per), jend = min(K, jbeg + per);
+  const int total = jend * vpr;
+  for (int e0 = jbeg * vpr + threadIdx.x; e0 < total; e0 += 4 * blockDim.x) {
     uint4 v[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
@@ -167,23 +177,36 @@ __global__ void __launch_bounds__(256) k_init_sample(XView q, XView k, int N, in
   }
 }
 
+// Anchor-prep arithmetic type.  fp32 (default): Gamma sums K_a <= 1024 products and W_j = Gamma c_j
+// 128 more, so W carries ~1e-6 relative error, below the 2^-17 resolution of its bf16 hi + lo split
+// that the assignment GEMM consumes; fp64 (-DCS_PREP_FP64) for A/B comparisons.
+#ifdef CS_PREP_FP64
+typedef double prep_t;
+typedef double2 prep2_t;
+__device__ __forceinline__ __nv_bfloat16 to_bf16(double v) { return __double2bfloat16(v); }
+#else
+typedef float prep_t;
+typedef float2 prep2_t;
+__device__ __forceinline__ __nv_bfloat16 to_bf16(float v) { return __float2bfloat16_rn(v); }
+#endif
+
 // ---------------------------------------------------------------------------------------------
-// a2: Gamma = C_a^T C_a (fp64).  grid (BH, NB (NB+1) / 2), block 256: one 64 x 64 block of the
+// a2: Gamma = C_a^T C_a (prep_t: fp32 by default, fp64 with -DCS_PREP_FP64).  grid (BH, NB (NB+1) / 2), block 256: one 64 x 64 block of the
 // upper triangle of Gamma per CTA (an off-diagonal block also writes its mirror: Gamma is
 // symmetric); thread (ti, tj) = (t / 16, t % 16) owns the 4 x 4 outputs (e0 + ti + 16 i,
-// f0 + tj + 16 j): the 16 lanes of a half-warp read 16 consecutive doubles (one wavefront) and
+// f0 + tj + 16 j): the 16 lanes of a half-warp read 16 consecutive elements (one wavefront for fp64) and
 // the two halves the same ones (broadcast).
 // Rows of C_a are staged in fp64 chunks of 32; per staged row 8 LDS.64 feed 16 DFMA.
 // ---------------------------------------------------------------------------------------------
 template <int D>
 __global__ void __launch_bounds__(256) k_gamma(const float* __restrict__ ca, int ka,
-                                               double* __restrict__ gamma) {
+                                               prep_t* __restrict__ gamma) {
   // split over the anchor rows: CTA z sums rows [z GR, (z+1) GR) into the partial Gamma_z (a
   // [gridDim.z][BH][D][D] slab); k_gamma_reduce adds the partials into slab 0 in a fixed order.
   // Short serial loops keep the kernel off the latency floor when few heads share a launch
   // (head-parallel ranks).
   constexpr int CH = 32, TB = 64, NB = D / TB, GR = kGammaRows;
-  __shared__ __align__(16) double sa[CH][D];
+  __shared__ __align__(16) prep_t sa[CH][D];
   // upper-triangle block index -> (row block, column block), column block >= row block
   int rb = 0, cb = blockIdx.y;
   while (cb >= NB - rb) { cb -= NB - rb; ++rb; }
@@ -193,11 +216,11 @@ __global__ void __launch_bounds__(256) k_gamma(const float* __restrict__ ca, int
   const float* A = ca + (size_t)bh * ka * D;
   gamma += (size_t)blockIdx.z * gridDim.x * D * D;
   const int t = threadIdx.x, ti = t >> 4, tj = t & 15;
-  double acc[4][4];
+  prep_t acc[4][4];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    for (int j = 0; j < 4; ++j) acc[i][j] = prep_t(0);
   for (int a0 = r_beg; a0 < r_end; a0 += CH) {
     const int n = min(CH, r_end - a0);
     __syncthreads();
@@ -208,7 +231,7 @@ __global__ void __launch_bounds__(256) k_gamma(const float* __restrict__ ca, int
     }
     __syncthreads();
     for (int r = 0; r < n; ++r) {
-      double ve[4], vf[4];
+      prep_t ve[4], vf[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) { ve[i] = sa[r][e0 + ti + 16 * i]; vf[i] = sa[r][f0 + tj + 16 * i]; }
 #pragma unroll
@@ -217,7 +240,7 @@ __global__ void __launch_bounds__(256) k_gamma(const float* __restrict__ ca, int
         for (int j = 0; j < 4; ++j) acc[i][j] = fma(ve[i], vf[j], acc[i][j]);
     }
   }
-  double* G = gamma + (size_t)bh * D * D;
+  prep_t* G = gamma + (size_t)bh * D * D;
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -231,59 +254,59 @@ __global__ void __launch_bounds__(256) k_gamma(const float* __restrict__ ca, int
 }
 
 // slab 0 += slabs 1 .. nparts-1 (fixed order: deterministic); grid ceil(BH D D / 2 / 256)
-__global__ void __launch_bounds__(256) k_gamma_reduce(double* __restrict__ gamma, size_t slab, int nparts) {
+__global__ void __launch_bounds__(256) k_gamma_reduce(prep_t* __restrict__ gamma, size_t slab, int nparts) {
   const size_t i = ((size_t)blockIdx.x * 256 + threadIdx.x) * 2;
   if (i >= slab) return;
-  double2 a = *reinterpret_cast<const double2*>(gamma + i);
+  prep2_t a = *reinterpret_cast<const prep2_t*>(gamma + i);
   for (int z = 1; z < nparts; ++z) {
-    const double2 b = *reinterpret_cast<const double2*>(gamma + (size_t)z * slab + i);
+    const prep2_t b = *reinterpret_cast<const prep2_t*>(gamma + (size_t)z * slab + i);
     a.x += b.x;
     a.y += b.y;
   }
-  *reinterpret_cast<double2*>(gamma + i) = a;
+  *reinterpret_cast<prep2_t*>(gamma + i) = a;
 }
 
 // ---------------------------------------------------------------------------------------------
 // a2: w_j = Gamma c_j (= (C_s Gamma)_j, Gamma symmetric), n_j^2 = ||c_j C_a^T||^2 = c_j . w_j,
 //     W_j = w_j / n_j  ->  Wsplit[bh][j] = [bf16(W) | bf16(W - bf16(W))]
-// grid (ks_pad / 32, BH), block 256, dyn smem 2 * 32 * D doubles: 32 centroids per CTA.
+// grid (ks_pad / 32, BH), block 256, dyn smem 2 * 32 * D prep_t: 32 centroids per CTA.
 // Thread (tj, te): centroids j0 + JPT tj .. +JPT-1, output columns te + EG e, e < 4 (EG = D/4;
 // consecutive lanes read consecutive Gamma columns).  Gamma is streamed through shared memory in chunks of 32 rows.  Rows j >= ks
 // are written as zeros (padding).
 // ---------------------------------------------------------------------------------------------
 template <int D>
 __global__ void __launch_bounds__(256) k_anchor_w(const float* __restrict__ cs_, int ks, int ks_pad,
-                                                  const double* __restrict__ gamma,
+                                                  const prep_t* __restrict__ gamma,
                                                   __nv_bfloat16* __restrict__ wsplit) {
   constexpr int J = 32, EG = D / 4, JG = 256 / EG, JPT = J / JG, FCH = 32;
-  extern __shared__ __align__(16) double sm_aw[];
-  double (*sc)[D] = reinterpret_cast<double (*)[D]>(sm_aw);           // [J][D]   centroids
-  double (*sg)[D] = reinterpret_cast<double (*)[D]>(sm_aw + J * D);   // [FCH][D] Gamma rows
+  extern __shared__ __align__(16) prep_t sm_aw[];
+  prep_t (*sc)[D] = reinterpret_cast<prep_t (*)[D]>(sm_aw);           // [J][D]   centroids
+  prep_t (*sg)[D] = reinterpret_cast<prep_t (*)[D]>(sm_aw + J * D);   // [FCH][D] Gamma rows
   const int bh = blockIdx.y, j0 = blockIdx.x * J, t = threadIdx.x;
   const int te = t % EG, tj = t / EG;
   const float* S = cs_ + (size_t)bh * ks * D;
-  const double* G = gamma + (size_t)bh * D * D;
+  const prep_t* G = gamma + (size_t)bh * D * D;
   for (int i = t; i < J * D / 4; i += 256) {
     const int r = i / (D / 4), c = (i % (D / 4)) * 4;
     float4 v = (j0 + r < ks) ? *reinterpret_cast<const float4*>(S + (size_t)(j0 + r) * D + c) : make_float4(0.f, 0.f, 0.f, 0.f);
     sc[r][c] = v.x; sc[r][c + 1] = v.y; sc[r][c + 2] = v.z; sc[r][c + 3] = v.w;
   }
-  double w[JPT][4];
+  prep_t w[JPT][4];
 #pragma unroll
   for (int i = 0; i < JPT; ++i)
 #pragma unroll
-    for (int e = 0; e < 4; ++e) w[i][e] = 0.0;
+    for (int e = 0; e < 4; ++e) w[i][e] = prep_t(0);
   for (int f0 = 0; f0 < D; f0 += FCH) {
     __syncthreads();
     for (int i = t; i < FCH * D / 2; i += 256) {
       const int r = i / (D / 2), c = (i % (D / 2)) * 2;
-      const double2 g = *reinterpret_cast<const double2*>(G + (size_t)(f0 + r) * D + c);
+      const prep2_t g = *reinterpret_cast<const prep2_t*>(G + (size_t)(f0 + r) * D + c);
       sg[r][c] = g.x; sg[r][c + 1] = g.y;
     }
     __syncthreads();
 #pragma unroll 4
     for (int f = 0; f < FCH; ++f) {
-      double g[4], c[JPT];
+      prep_t g[4], c[JPT];
 #pragma unroll
       for (int e = 0; e < 4; ++e) g[e] = sg[f][te + EG * e];
 #pragma unroll
@@ -299,7 +322,7 @@ __global__ void __launch_bounds__(256) k_anchor_w(const float* __restrict__ cs_,
 #pragma unroll
   for (int i = 0; i < JPT; ++i) {
     const int jl = JPT * tj + i, j = j0 + jl;
-    double n2 = 0.0;
+    prep_t n2 = prep_t(0);
 #pragma unroll
     for (int e = 0; e < 4; ++e) n2 = fma(sc[jl][te + EG * e], w[i][e], n2);
 #pragma unroll
@@ -308,12 +331,12 @@ __global__ void __launch_bounds__(256) k_anchor_w(const float* __restrict__ cs_,
     __nv_bfloat16* out = wsplit + ((size_t)bh * ks_pad + j) * (2 * D);
     __nv_bfloat16 hi[4], lo[4];
     if (j < ks) {
-      const double inv = n2 > 0.0 ? 1.0 / sqrt(n2) : 0.0;  // ||Pbar_j|| = 0 -> W_j = 0
+      const prep_t inv = n2 > prep_t(0) ? prep_t(1) / sqrt(n2) : prep_t(0);  // ||Pbar_j|| = 0 -> W_j = 0
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const double wv = w[i][e] * inv;
-        hi[e] = __double2bfloat16(wv);
-        lo[e] = __double2bfloat16(wv - (double)__bfloat162float(hi[e]));
+        const prep_t wv = w[i][e] * inv;
+        hi[e] = to_bf16(wv);
+        lo[e] = to_bf16(wv - (prep_t)__bfloat162float(hi[e]));
       }
     } else {
 #pragma unroll
@@ -595,23 +618,28 @@ __global__ void __launch_bounds__(256) k_permute_rows(XView x, int N, int d,
 cudaError_t launch_init_sample(XView q, XView k, int BH, int N, int d, int kq, int kk,
                                unsigned long long seed, int h_off, int h_tot, const int32_t* init_q,
                                const int32_t* init_k, float* cq, float* ck, cudaStream_t st) {
-  const size_t smem = (size_t)((N + 31) / 32) * 4 + (size_t)max(kq, kk) * 8 + 32 * 4;  // bitmap, draws, picks, flags
+  const size_t smem = (size_t)(((N + 31) / 32 + 3) & ~3) * 4 + (size_t)max(kq, kk) * 8 + 32 * 4;  // bitmap, draws, picks, flags
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k_init_sample, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
   }
-  k_init_sample<<<dim3(BH, 2), 256, smem, st>>>(q, k, N, d, kq, kk, seed, h_off, h_tot, init_q, init_k,
-                                                cq, ck);
+  // gather parts per (bh, side): about two CTAs per SM in total (the sampling is recomputed per
+  // part: ~K^2/4 broadcast compares, cheap next to the row gather it parallelises)
+  int G = (2 * 148 + 2 * BH - 1) / (2 * BH);
+  G = G < 1 ? 1 : (G > 16 ? 16 : G);
+  k_init_sample<<<dim3(BH, 2, G), 256, smem, st>>>(q, k, N, d, kq, kk, seed, h_off, h_tot, init_q, init_k,
+                                                   cq, ck);
   return cudaGetLastError();
 }
 
 cudaError_t launch_anchor_prep(const float* ca, int ka, const float* cself, int ks, int ks_pad,
-                               int BH, int d, double* gamma, __nv_bfloat16* wsplit, cudaStream_t st) {
+                               int BH, int d, void* gamma_ws, __nv_bfloat16* wsplit, cudaStream_t st) {
+  prep_t* gamma = static_cast<prep_t*>(gamma_ws);
   const int nparts = (ka + kGammaRows - 1) / kGammaRows;  // gamma holds nparts x BH x d x d
   const size_t slab = (size_t)BH * d * d;
   if (d == 128) {
-    constexpr int smem = 2 * 32 * 128 * 8;
+    constexpr int smem = 2 * 32 * 128 * (int)sizeof(prep_t);
     cudaError_t e = cudaFuncSetAttribute(k_anchor_w<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     k_gamma<128><<<dim3(BH, 3, nparts), 256, 0, st>>>(ca, ka, gamma);
@@ -620,7 +648,7 @@ cudaError_t launch_anchor_prep(const float* ca, int ka, const float* cself, int 
   } else {
     k_gamma<64><<<dim3(BH, 1, nparts), 256, 0, st>>>(ca, ka, gamma);
     if (nparts > 1) k_gamma_reduce<<<(unsigned)((slab / 2 + 255) / 256), 256, 0, st>>>(gamma, slab, nparts);
-    k_anchor_w<64><<<dim3((ks_pad + 31) / 32, BH), 256, 2 * 32 * 64 * 8, st>>>(cself, ks, ks_pad, gamma, wsplit);
+    k_anchor_w<64><<<dim3((ks_pad + 31) / 32, BH), 256, 2 * 32 * 64 * (int)sizeof(prep_t), st>>>(cself, ks, ks_pad, gamma, wsplit);
   }
   return cudaGetLastError();
 }

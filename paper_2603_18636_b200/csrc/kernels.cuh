@@ -30,7 +30,8 @@ cudaError_t launch_init_sample(XView q, XView k, int BH, int N, int d, int kq, i
                                unsigned long long seed, int h_off, int h_tot, const int32_t* init_q,
                                const int32_t* init_k, float* cq, float* ck, cudaStream_t st);
 cudaError_t launch_anchor_prep(const float* ca, int ka, const float* cself, int ks, int ks_pad,
-                               int BH, int d, double* gamma, __nv_bfloat16* wsplit, cudaStream_t st);
+                               int BH, int d, void* gamma_ws /*fp64-sized scratch*/, __nv_bfloat16* wsplit,
+                               cudaStream_t st);
 // k-means baseline (NEXT-2): Wsplit[bh][j] = [bf16(c_j) | bf16(c_j - bf16(c_j))], bias = -||c_j||^2 / 2
 cudaError_t launch_kmeans_prep(const float* cself, int ks, int ks_pad, int BH, int d, __nv_bfloat16* wsplit,
                                float* bias, cudaStream_t st);
