@@ -127,8 +127,9 @@ class ClockSampler:
         mx = max(float(r[2]) for r in rows if r[2].replace(".", "").isdigit())
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        pw = sorted(float(r[3]) for r in rows if r[3].replace(".", "").isdigit())
         return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
-                "samples": len(rows)}
+                "power_w": pw[len(pw) // 2] if pw else None, "samples": len(rows)}
 
 
 # ------------------------------------------------------------------------------ oracle baseline

@@ -29,7 +29,7 @@ namespace attn {
 // event trace of one CTA (blockIdx 0,0): t[event][tile] = clock64 (debug variant only)
 __device__ long long g_trace[20][4096];
 // per-CTA timeline (debug variant): [cta][0] entry globaltimer, [1] after setup, [2] first S seen,
-// [3] exit, [4] smid, [5] nt
+// [3] exit, [4] smid, [5] nt, [6] clock64 at entry, [7] clock64 at exit
 __device__ long long g_cta[65536][8];
 __device__ __forceinline__ long long gtimer() {
   long long t;
@@ -113,6 +113,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   float* xch = reinterpret_cast<float*>(sm + L::OFF_XCH);
 
   CS_CTA(0, gtimer());
+  CS_CTA(6, clock64());
   const int bh = blockIdx.y;
   const int item = blockIdx.x;
   const int32_t* ist = item_start + (size_t)bh * (kq + 1);
@@ -159,7 +160,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   }
   if (warp == WARP_MMA) {
     tmem_alloc(reinterpret_cast<uint32_t*>(misc), 512);
-    CS_CTA_W(6, gtimer());  // TMEM allocated
+
   }
   if (warp == WARP_PRODUCER) {
     const int n = n_rows ? n_rows[(size_t)bh * kq + a] : n_keep[bh];  // per-row counts (R11b)
@@ -195,7 +196,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
     }
     if (lane == 0) { ucum[n] = carry; misc[1] = carry; misc[2] = n; }
-    CS_CTA_W(7, gtimer());  // unit table built
+
   }
   tc_fence_before();
   __syncthreads();
@@ -608,6 +609,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     tmem_dealloc(tmem, 512);
   }
   CS_CTA(3, gtimer());
+  CS_CTA(7, clock64());
 }
 
 }  // namespace attn

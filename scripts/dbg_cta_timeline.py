@@ -22,8 +22,9 @@ first = (v[:, 2] - v[:, 1]) / 1e3
 print("CTA duration us: median %.1f  mean %.1f" % (np.median(dur), dur.mean()))
 print("setup (entry -> tables/TMEM ready) us: median %.2f mean %.2f" % (np.median(setup), setup.mean()))
 print("ready -> first S tile us: median %.2f mean %.2f" % (np.median(first), first.mean()))
-print("  entry -> TMEM allocated us: median %.2f; entry -> unit table built us: median %.2f" %
-      (np.median((v[:, 6] - v[:, 0]) / 1e3), np.median((v[:, 7] - v[:, 0]) / 1e3)))
+ghz = (v[:, 7] - v[:, 6]) / (v[:, 3] - v[:, 0])
+print("effective SM clock GHz (clock64 / globaltimer over each CTA): median %.3f  p10 %.3f  p90 %.3f" %
+      (np.median(ghz), np.percentile(ghz, 10), np.percentile(ghz, 90)))
 nt = v[:, 5] & 0xfffff
 sp = (v[:, 5] >> 20) & 1
 loop = dur - setup - first
@@ -31,8 +32,9 @@ print("per-KV-tile loop us: median %.3f" % np.median(loop / np.maximum(nt, 1)))
 for flag, name in ((0, "pair items"), (1, "split-KV single-tile items")):
     m = sp == flag
     if m.any():
-        print(f"{name}: {m.sum()} CTAs, per-KV-tile us median %.3f, duration median %.1f" %
-              (np.median(loop[m] / np.maximum(nt[m], 1)), np.median(dur[m])))
+        print(f"{name}: {m.sum()} CTAs, per-KV-tile us median %.3f (cycles %.0f), duration median %.1f" %
+              (np.median(loop[m] / np.maximum(nt[m], 1)), np.median(loop[m] * 1e3 * ghz[m] / np.maximum(nt[m], 1)),
+               np.median(dur[m])))
 gaps = []
 for sm in np.unique(v[:, 4]):
     x = v[v[:, 4] == sm]

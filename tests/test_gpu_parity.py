@@ -421,6 +421,45 @@ def test_attn_singleton_keys_pick_value(pb):
     assert torch.equal(O[0, 0].cpu(), exp)
 
 
+@pytest.mark.parametrize("order", ["rising", "falling"])
+def test_attn_max_jumps_within_tiles(pb, order):
+    """The online softmax's rescaling paths (attn.cu: P(j) is computed against the running max of
+    the earlier tiles; a tile whose max grows by > 8 in the log2 domain moves the reference for the
+    next tile; a jump so large that a P half's row sum would exceed 2^40 is recomputed mid-tile,
+    in the first or the second 64-key half).  One key cluster of 1024 keys in token order (8 key
+    tiles); the score level q.k ~ 128 g steps up inside tile 1's second half (g = 3, a jump of ~49
+    in the log2 domain), at tile 2's first half (g = 6), by a moderate 0.7 at tile 4 (~11), and is
+    random below the maximum afterwards.  Query clusters of 100 rows (one split-KV item) and 924
+    rows (pair items plus one split-KV item); every query keeps the only key cluster."""
+    d, N = 128, 1024
+    gen = torch.Generator().manual_seed(11)
+    g = np.zeros(N)
+    g[192:256] = 3.0
+    g[256:512] = 6.0
+    g[512:640] = 6.7
+    g[640:] = np.random.default_rng(3).uniform(0.0, 6.7, N - 640)
+    if order == "falling":
+        g = g[::-1].copy()
+    u = torch.ones(d)
+    q = (u + 0.5 * torch.randn(N, d, generator=gen)).to(torch.bfloat16)
+    k = (torch.from_numpy(g).float()[:, None] * u + 0.3 * torch.randn(N, d, generator=gen)).to(torch.bfloat16)
+    v = torch.randn(N, d, generator=gen).to(torch.bfloat16)
+    Lq = np.where(np.arange(N) % 10 == 0, 0, 1)  # 103 / 921 rows
+    Lk = np.zeros(N, np.int64)
+    pq, oq = svoo.counting_sort(Lq, 2)
+    pk, ok = svoo.counting_sort(Lk, 1)
+    kept = np.zeros((2, 1), np.int64)
+    t = lambda a: torch.from_numpy(np.asarray(a).astype(np.int32))
+    O = pb.block_sparse_attn(q[None, None].cuda(), k[None, None].cuda(), v[None, None].cuda(),
+                             t(pq)[None, None].cuda(), t(oq)[None, None].cuda(), t(pk)[None, None].cuda(),
+                             t(ok)[None, None].cuda(), torch.ones(1, 1, dtype=torch.int32).cuda(),
+                             t(kept)[None, None].cuda())
+    ref = svoo.sparse_attention(f64(q), f64(k), f64(v), Lq, Lk, kept)
+    err = np.abs(f64(O[0, 0]) - ref)
+    assert np.isfinite(f64(O[0, 0])).all()
+    assert err.max() <= ATOL_MAX and err.mean() <= ATOL_MEAN, (err.max(), err.mean())
+
+
 # ------------------------------------------------------------------------- P6 end to end
 def test_fused_toy_end_to_end(pb):
     """P6 on the toy config: the first sampler seed whose oracle run has no near-tie in any
