@@ -34,6 +34,12 @@ __global__ void k(float* out, long long* cyc, int iters) {
         u[i] ^= h;
         a[i] = fadd2(a[i], make_float2(__uint_as_float(h << 16), __uint_as_float(h & 0xffff0000u)));
       }
+      if (MODE == 12) {  // the attention's pair mix: 3 of 4 pairs on MUFU, 1 on the polynomial
+        const float2 x = ffma2(a[i], c2, d2);
+        const float2 p = (i & 3) == 3 ? ex2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
+        a[i] = fadd2(a[i], p);
+        u[i] ^= pack_bf16x2(p.x, p.y);
+      }
       if (MODE == 11) {  // current pair: ffma2, 2x ex2 f32, fadd2, pack
         const float2 x = ffma2(a[i], c2, d2);
         const float2 p = make_float2(ex2(x.x), ex2(x.y));
@@ -65,11 +71,11 @@ void run(const char* name, int warps) {
 }
 
 int main() {
-  for (int w : {4, 8, 16}) {
+  for (int w : {4, 8, 16, 32}) {
     run<0>("mufu.ex2", w); run<1>("ffma2", w); run<2>("fadd2", w); run<3>("f2fp", w);
     run<4>("ffma", w); run<5>("fmnmx3", w); run<6>("poly2", w);
     run<7>("ex2.bf16x2", w); run<8>("ex2.f16x2", w); run<9>("cvt.bf16x2", w);
-    run<10>("pair.bf16", w); run<11>("pair.f32", w);
+    run<10>("pair.bf16", w); run<11>("pair.f32", w); run<12>("pair.mix", w);
   }
   return 0;
 }
