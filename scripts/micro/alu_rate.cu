@@ -55,6 +55,47 @@ __global__ void k(float* out, long long* cyc, int iters) {
   if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
 }
 
+// One row's worth of softmax pairs per iteration: NP independent pairs (x from a register array),
+// the kernel's mix (3 of 4 pairs on MUFU, 1 on the polynomial), 4 FADD2 sum chains, bf16 pack.
+template <int NP>
+__global__ void k_wide(float* out, long long* cyc, int iters) {
+  float2 s[NP];
+  for (int i = 0; i < NP; ++i) s[i] = make_float2(-(threadIdx.x & 7) * 0.1f - i * 0.01f, -i * 0.02f);
+  float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+  uint32_t pk = 0;
+  const float2 sl2 = make_float2(0.1275f, 0.1275f);
+  float m = 0.f;
+  __syncthreads();
+  long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+    const float2 nm2 = make_float2(-m, -m);
+#pragma unroll
+    for (int c = 0; c < NP; ++c) {
+      const float2 x = ffma2(s[c], sl2, nm2);
+      const float2 p = (c & 3) == 3 ? ex2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
+      acc[c & 3] = fadd2(acc[c & 3], p);
+      pk ^= pack_bf16x2(p.x, p.y);
+    }
+    m += 1e-7f * acc[0].x;  // next iteration depends on this one (like the next tile on the max)
+  }
+  long long t1 = clock64();
+  out[blockIdx.x * blockDim.x + threadIdx.x] = acc[0].x + acc[1].y + acc[2].x + acc[3].y + (float)pk;
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+template <int NP>
+void run_wide(int warps) {
+  float* out; long long* cyc;
+  cudaMalloc(&out, 1024 * 4 * 148); cudaMalloc(&cyc, 8 * 148);
+  const int iters = 1024;
+  k_wide<NP><<<148, warps * 32>>>(out, cyc, 16);
+  k_wide<NP><<<148, warps * 32>>>(out, cyc, iters);
+  long long c = 0;
+  cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
+  printf("wide NP=%2d warps=%2d  cycles per pair per SMSP: %.2f  (per row of %d pairs per warp: %.0f)\n", NP, warps,
+         (double)c / (iters * (double)NP) / (warps / 4.0), NP, (double)c / iters);
+  cudaFree(out); cudaFree(cyc);
+}
+
 template <int MODE>
 void run(const char* name, int warps) {
   float* out; long long* cyc;
@@ -70,7 +111,11 @@ void run(const char* name, int warps) {
   cudaFree(out); cudaFree(cyc);
 }
 
-int main() {
+int main(int argc, char** argv) {
+  if (argc > 1) {
+    for (int w : {4, 8, 16}) { run_wide<16>(w); run_wide<32>(w); run_wide<64>(w); }
+    return 0;
+  }
   for (int w : {4, 8, 16, 32}) {
     run<0>("mufu.ex2", w); run<1>("ffma2", w); run<2>("fadd2", w); run<3>("f2fp", w);
     run<4>("ffma", w); run<5>("fmnmx3", w); run<6>("poly2", w);
