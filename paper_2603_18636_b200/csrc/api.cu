@@ -332,9 +332,10 @@ cs_status run_attn(int B, int H, int N, int d, int kq, int kk, const int32_t* pe
   CUtensorMap tq;
   KVMaps kv;
   CS_CHECK(make_map_2d(&tq, sc.qp, (uint64_t)BH * N, d, 128));
-  for (int i = 0; i < 5; ++i) {  // box heights 8..128 rows
-    CS_CHECK(make_map_2d(&kv.k[i], sc.kp, (uint64_t)BH * N, d, 8u << i));
-    CS_CHECK(make_map_2d(&kv.v[i], sc.vp, (uint64_t)BH * N, d, 8u << i));
+  for (int i = 0; i < kKVBoxes; ++i) {  // box heights 8, 16, .., 128 rows (i < 5), then 1..7 rows
+    const uint32_t rows = i < 5 ? 8u << i : (uint32_t)(i - 4);
+    CS_CHECK(make_map_2d(&kv.k[i], sc.kp, (uint64_t)BH * N, d, rows));
+    CS_CHECK(make_map_2d(&kv.v[i], sc.vp, (uint64_t)BH * N, d, rows));
   }
   if (ev) CS_CUDA(record_stage_event(ev[2], st), "event");
   CS_CUDA(launch_bsa_fwd(&tq, &kv, BH, H, N, d, kq, kk, perm_q, offs_q, offs_k, n_keep, n_rows, kept,

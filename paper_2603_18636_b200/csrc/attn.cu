@@ -53,7 +53,7 @@ __device__ __forceinline__ int smid() {
 #define CS_CTA_W(e, v)
 #endif
 
-constexpr int BM = 128, BN = 128, UNIT = 8, UPT = BN / UNIT, NST = 2;
+constexpr int BM = 128, BN = 128, NST = 2;
 constexpr int NTHREADS = 352;
 constexpr int WARP_PRODUCER = 8, WARP_MMA = 9, WARP_VLOAD = 10;
 constexpr float kRescaleThresh = 8.0f;
@@ -74,12 +74,10 @@ struct Smem {
   static constexpr int OFF_V = OFF_K + NST * KT;
   static constexpr int OFF_BAR = OFF_V + NST * KT;
   // q_full, k_full[2], k_empty[2], v_full[2], v_empty[2], s_full[2], p_full[2 tiles][2 halves], o_full
-  static constexpr int OFF_MISC = OFF_BAR + 16 * 8;  // tmem slot, U, n
-  static constexpr int OFF_UROW = OFF_MISC + 16;      // [NST][UPT] unit start rows
-  static constexpr int OFF_KSTART = OFF_UROW + NST * UPT * 4;
-  static constexpr int OFF_KLEN = OFF_KSTART + kMaxClusters * 4;
-  static constexpr int OFF_UCUM = OFF_KLEN + kMaxClusters * 4;
-  static constexpr int OFF_XCH = OFF_UCUM + ((kMaxClusters + 1) * 4 + 15) / 16 * 16;
+  static constexpr int OFF_MISC = OFF_BAR + 16 * 8;  // tmem slot, R, n
+  static constexpr int OFF_KSTART = OFF_MISC + 16;    // [n] first sorted row of kept cluster i
+  static constexpr int OFF_RCUM = OFF_KSTART + kMaxClusters * 4;  // [n + 1] row prefix sums
+  static constexpr int OFF_XCH = OFF_RCUM + ((kMaxClusters + 1) * 4 + 15) / 16 * 16;
   static constexpr int BYTES = OFF_XCH + 4 * BM * 4;  // split-KV merge: m[2][BM], l[2][BM]
   static constexpr int ALLOC = BYTES + 1024;  // room to align the base to 1024
 };
@@ -108,8 +106,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint64_t* o_full = bars + 15;
   int* misc = reinterpret_cast<int*>(sm + L::OFF_MISC);
   int* kstart = reinterpret_cast<int*>(sm + L::OFF_KSTART);
-  int* klen = reinterpret_cast<int*>(sm + L::OFF_KLEN);
-  int* ucum = reinterpret_cast<int*>(sm + L::OFF_UCUM);
+  int* rcum = reinterpret_cast<int*>(sm + L::OFF_RCUM);
   float* xch = reinterpret_cast<float*>(sm + L::OFF_XCH);
 
   CS_CTA(0, gtimer());
@@ -156,7 +153,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           tma_load_2d(sm + L::OFF_Q + tq * L::QT + hf * L::HALF_Q, &tm_q, hf * 64,
                       bh * N + qbeg + (t0 + tq) * BM, q_full);
     }
-    if (lane < 5) { tma_prefetch_desc(&kv.k[lane]); tma_prefetch_desc(&kv.v[lane]); }
+    if (lane < kKVBoxes) { tma_prefetch_desc(&kv.k[lane]); tma_prefetch_desc(&kv.v[lane]); }
   }
   if (warp == WARP_MMA) {
     tmem_alloc(reinterpret_cast<uint32_t*>(misc), 512);
@@ -185,26 +182,25 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int i = i0 + 32 * u + lane;
-        const int len = en4[u] - st4[u];
-        const int nu = i < n ? (len + UNIT - 1) / UNIT : 0;
-        if (i < n) { kstart[i] = st4[u]; klen[i] = len; }
-        int x = nu;
+        const int len = i < n ? en4[u] - st4[u] : 0;
+        if (i < n) kstart[i] = st4[u];
+        int x = len;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) { int y = __shfl_up_sync(0xffffffffu, x, o); if (lane >= o) x += y; }
-        if (i < n) ucum[i] = carry + x - nu;
+        if (i < n) rcum[i] = carry + x - len;
         carry += __shfl_sync(0xffffffffu, x, 31);
       }
     }
-    if (lane == 0) { ucum[n] = carry; misc[1] = carry; misc[2] = n; }
+    if (lane == 0) { rcum[n] = carry; misc[1] = carry; misc[2] = n; }
 
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = static_cast<uint32_t>(misc[0]);
-  const int U = misc[1];
+  const int R = misc[1];  // kept key rows, packed back to back into 128-key tiles
   const int nkeep = misc[2];
-  const int nt = (U + UPT - 1) / UPT;
+  const int nt = (R + BN - 1) / BN;
   CS_CTA(1, gtimer());
   CS_CTA(4, smid());
   CS_CTA(5, nt | (split ? (1 << 20) : 0));
@@ -212,42 +208,46 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   if (warp == WARP_PRODUCER || warp == WARP_VLOAD) {
     // ================= TMA producers: warp 8 -> Q and K(j), warp 10 -> V(j) =================
     const bool is_v = warp == WARP_VLOAD;
-    // Unit rows of tile jj, computed by lanes 0..UPT-1 (lane u <-> unit u of the tile) with a
-    // cursor over the kept clusters (clusters are visited in order: usually 0-1 steps).
-    int cur = 0;  // kept-cluster index of the first unit of the current tile (warp-uniform)
-    auto unit_row = [&](int jj) -> int {
-      const int g = jj * UPT + lane;
-      while (cur + 1 < nkeep && ucum[cur + 1] <= jj * UPT) ++cur;
-      int i = cur, row = bh * N + kstart[0];
-      if (lane < UPT && g < U) {
-        while (i + 1 < nkeep && ucum[i + 1] <= g) ++i;
-        row = bh * N + kstart[i] + (g - ucum[i]) * UNIT;
-      }
-      return row;
-    };
-    // Issue one K or V tile: each lane that starts a run of row-contiguous units issues the
-    // power-of-two boxes covering its run (multi-lane TMA issue).
-    auto issue_tile = [&](uint64_t* bar, uint8_t* base, int row) {
-      const int prev = __shfl_up_sync(0xffffffffu, row, 1);
-      const bool start = lane < UPT && (lane == 0 || row != prev + UNIT);
-      const uint32_t starts = __ballot_sync(0xffffffffu, start) | (1u << UPT);
+    // Tile jj holds the kept rows [BN jj, BN jj + BN) of the concatenation of the kept clusters (in
+    // ascending cluster order).  Lane l takes the l-th cluster overlapping the tile (32 at a time)
+    // and issues the power-of-two row boxes (8..128 and 1..7 rows x 64 columns, SWIZZLE_128B: a box written
+    // at any 128-byte row offset lands in the tile's swizzled layout, scripts/micro/
+    // tma_rowbox_test.cu) that cover its segment; the last tile's rows past R are filled from the
+    // head's first rows (finite values; masked to -inf in the softmax).
+    int cur = 0;  // first kept cluster overlapping the current tile (warp-uniform)
+    auto issue_tile = [&](uint64_t* bar, uint8_t* base, int jj) {
+      const int t_beg = jj * BN, t_end = t_beg + BN;
       if (lane == 0) mbar_arrive_expect_tx(bar, L::KT);
       __syncwarp();
-      if (start) {
-        const uint32_t after = starts & ~((2u << lane) - 1u);  // run starts after this lane
-        const int len = __ffs(after) - 1 - lane;
+      // boxes of 128 .. 8 rows (maps 4 .. 0) for the multiple of 8, one box of 1..7 rows (map 4 + r)
+      // for the remainder
+      auto boxes = [&](int trow, int grow, int len) {
         int off = 0;
-#pragma unroll
+#pragma unroll 1
         for (int bi = 4; bi >= 0; --bi) {
-          if (len & (1 << bi)) {
-            const CUtensorMap* m = is_v ? &kv.v[bi] : &kv.k[bi];
+          if (len & (8 << bi)) {
 #pragma unroll
             for (int hf = 0; hf < L::HALVES; ++hf)
-              tma_load_2d(base + hf * L::HALF_K + (lane + off) * 1024, m, hf * 64, row + off * UNIT, bar);
-            off += 1 << bi;
+              tma_load_2d(base + hf * L::HALF_K + (trow + off) * 128, is_v ? &kv.v[bi] : &kv.k[bi], hf * 64, grow + off, bar);
+            off += 8 << bi;
           }
         }
+        if (len & 7) {
+          const int bi = 4 + (len & 7);
+#pragma unroll
+          for (int hf = 0; hf < L::HALVES; ++hf)
+            tma_load_2d(base + hf * L::HALF_K + (trow + off) * 128, is_v ? &kv.v[bi] : &kv.k[bi], hf * 64, grow + off, bar);
+        }
+      };
+      while (cur < nkeep && rcum[cur + 1] <= t_beg) ++cur;
+      for (int i0 = cur; i0 < nkeep && rcum[i0] < t_end; i0 += 32) {
+        const int i = i0 + lane;
+        if (i < nkeep && rcum[i] < t_end) {
+          const int s0 = max(rcum[i], t_beg), s1 = min(rcum[i + 1], t_end);
+          if (s1 > s0) boxes(s0 - t_beg, bh * N + kstart[i] + (s0 - rcum[i]), s1 - s0);
+        }
       }
+      if (lane == 0 && t_end > R) boxes(R - t_beg, bh * N, t_end - R);
       __syncwarp();
     };
     uint64_t* full = is_v ? v_full : k_full;
@@ -255,10 +255,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     uint8_t* ring = sm + (is_v ? L::OFF_V : L::OFF_K);
     for (int jj = 0; jj < nt; ++jj) {
       const int slot = jj % NST;
-      const int row = unit_row(jj);
       mbar_wait(empty + slot, ((jj / NST) & 1) ^ 1);
       if (lane == 0) CS_TRACE(is_v ? 10 : 9, jj);
-      issue_tile(full + slot, ring + slot * L::KT, row);
+      issue_tile(full + slot, ring + slot * L::KT, jj);
       if (lane == 0) CS_TRACE(is_v ? 1 : 0, jj);
     }
   } else if (warp == WARP_MMA) {
@@ -426,40 +425,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const uint32_t s_tm = tmem + lane_off + tq * 128;
       const uint32_t o_tm = tmem + lane_off + 256 + tq * 128;
       float m = -INFINITY, l = 0.f;
-      // invalid columns of tile j (warp-uniform): rows past each kept cluster's end in its last
-      // unit, and the padding units after the last kept cluster.  Computed one tile ahead, while
-      // the warp waits for the next S, so it is off the softmax critical path.
-      int ci = 0;  // cursor over kept clusters: the next one whose last unit is not yet masked
+      // invalid columns: only the last tile's, past the R kept rows (the tiles are row-exact)
       uint32_t mw0 = 0, mw1 = 0, mw2 = 0, mw3 = 0;
       auto tile_mask = [&](int j) {
-        mw0 = mw1 = mw2 = mw3 = 0;
-        const int g0 = j * UPT;
-        while (ci < nkeep) {
-          const int gl = ucum[ci + 1] - 1;  // last unit of kept cluster ci
-          if (gl >= g0 + UPT) break;
-          const int vc = klen[ci] - UNIT * (gl - ucum[ci]);
-          if (vc < UNIT && gl >= ucum[ci] && gl >= g0) {  // (split: may end in a skipped tile)
-            const int u = gl - g0;
-            const uint32_t bits = ((0xffu << vc) & 0xffu) << (8 * (u & 3));
-            const int w = u >> 2;
-            mw0 |= w == 0 ? bits : 0u; mw1 |= w == 1 ? bits : 0u;
-            mw2 |= w == 2 ? bits : 0u; mw3 |= w == 3 ? bits : 0u;
-          }
-          ++ci;
-        }
-        if (g0 + UPT > U) {
-          for (int u = U - g0; u < UPT; ++u) {
-            const uint32_t bits = 0xffu << (8 * (u & 3));
-            const int w = u >> 2;
-            mw0 |= w == 0 ? bits : 0u; mw1 |= w == 1 ? bits : 0u;
-            mw2 |= w == 2 ? bits : 0u; mw3 |= w == 3 ? bits : 0u;
-          }
-        }
+        const int v = R - j * BN;  // valid columns of tile j
+        auto word = [&](int w) -> uint32_t {
+          const int c = v - 32 * w;
+          return c >= 32 ? 0u : (c <= 0 ? 0xffffffffu : (0xffffffffu << c));
+        };
+        mw0 = word(0); mw1 = word(1); mw2 = word(2); mw3 = word(3);
       };
-#ifdef CS_ATTN_DEBUG
-      float dbg_s0_keep = 0.f, dbg_s1_keep = 0.f;
-      uint32_t dbg_mw0_keep = 0;
-#endif
       tile_mask(split ? tq : 0);
       for (int j = 0; j < my_nt; ++j) {
         mbar_wait(s_full + tq, j & 1);
@@ -478,9 +453,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         CS_APPLY_MASK(1, mw1)
         CS_APPLY_MASK(2, mw2)
         CS_APPLY_MASK(3, mw3)
-#ifdef CS_ATTN_DEBUG
-        if (j == 0) { dbg_s0_keep = __uint_as_float(su[0]); dbg_s1_keep = __uint_as_float(su[1]); dbg_mw0_keep = mw0; }
-#endif
         CS_TRACE(16 + tq, j);
         // row max of the raw scores: 8 independent 3-input max chains
         float mx8[8];

@@ -68,10 +68,12 @@ cudaError_t launch_worklist(int BH, int kq, const int32_t* offs_q, int32_t* item
 int worklist_upper_bound(int N, int kq);
 
 // ---- attn.cu : block-sparse flash attention over cluster-sorted Q/K/V (bf16 [BH, N, d])
-// K/V maps over the sorted copies with box heights 8 << i rows (i = 0..4), box width 64 columns
+// K/V maps over the sorted copies, box width 64 columns, box heights kKVBoxRows[i]: 1..7 rows (a
+// segment's remainder below 8) and 8 << i (i = 0..4)
+constexpr int kKVBoxes = 12;
 struct KVMaps {
-  CUtensorMap k[5];
-  CUtensorMap v[5];
+  CUtensorMap k[kKVBoxes];
+  CUtensorMap v[kKVBoxes];
 };
 cudaError_t launch_bsa_fwd(const CUtensorMap* tm_q, const KVMaps* kv,
                            int BH, int H, int N, int d, int kq, int kk, const int32_t* perm_q,
