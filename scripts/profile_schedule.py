@@ -53,10 +53,10 @@ def main():
             t_prof.append(e0.elapsed_time(e1))
             dens[x, layer] = d[0].cpu().numpy()
             del w
-    sched = profiler.fit_schedule(dens)
+    sched = profiler.fit_schedule(dens, alpha=0.95, tau=a.tau)
     N = c["T"] * c["Hs"] * c["Ws"]
     meta = {"config": a.config, "N": N, "H": c["H"], "layers": L, "inputs": a.inputs, "tau": a.tau,
-            "passes": a.passes, "z": profiler.Z_ALPHA_95,
+            "passes": a.passes, "z": sched["z"],
             "ms_per_layer_profile_mean": float(np.mean(t_prof)), "ms_per_layer_profile_max": float(np.max(t_prof)),
             "density_mean": float(dens.mean()), "density_min": float(dens.min()), "density_max": float(dens.max()),
             "d_hat_mean": float(sched["d_hat"].mean()),

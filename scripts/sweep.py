@@ -29,6 +29,7 @@ import numpy as np
 import torch
 
 import paper_2603_18636_b200 as pb
+from paper_2603_18636_b200 import profiler
 from synthetic import CONFIGS, synthetic_profile, video_qkv
 
 RULES = {"density": 0, "as_written": 1, "fixed": 2}
@@ -184,7 +185,9 @@ def run_layers(a):
     c = CONFIGS[a.config]
     nl = a.layers
     if a.schedule:  # d_hat from the offline profiler (scripts/profile_schedule.py, NEXT-3)
-        prof = torch.tensor(json.load(open(a.schedule))["d_hat"], dtype=torch.float32)[:nl]
+        doc = json.load(open(a.schedule))
+        d_hat = profiler.load_schedule(doc)["d_hat"] if "entries" in doc else doc["d_hat"]  # r01 files: dense arrays
+        prof = torch.tensor(d_hat, dtype=torch.float32)[:nl]
     else:
         prof = synthetic_profile(nl, c["H"], seed=a.seed)  # [L, H]; layer 0 dense
     sust, _ = peaks()

@@ -135,3 +135,28 @@ def test_splitmix64_seed0_published_sequence():
     for o in outs:
         s, v = svoo.splitmix64_next(s)
         assert v == o
+
+
+def test_empty_cluster_keeps_centroid_effective_k():
+    """R5: an empty cluster keeps its previous centroid (it may attract tokens again
+    later) and is excluded from selection while empty.  The reference SPEC's CPU program instead
+    reseeds it from the farthest token before the next assignment; here the effective count at
+    selection is K_k' < K_k.  Construction: two keys are identical and both drawn as initial key
+    centroids, so the higher index loses every tie (R2) in the first Step A."""
+    rng = np.random.default_rng(7)
+    Q = rng.normal(size=(40, 4))
+    K = rng.normal(size=(40, 4))
+    K[11] = K[5]
+    init_k = np.array([5, 11, 20, 30])
+    init_q = np.array([0, 10, 20])
+    r1 = svoo.cocluster(Q, K, 3, 4, 1, init_q=init_q, init_k=init_k)
+    sizes_k = np.bincount(r1.Lk, minlength=4)
+    assert sizes_k[1] == 0 and np.array_equal(r1.Ck[1], K[11])   # empty, centroid kept (R5)
+    sizes_q = np.bincount(r1.Lq, minlength=3)
+    sel = svoo.select_blocks(r1.Cq, r1.Ck, sizes_q, sizes_k, 1.0, 0.95, 0.1, svoo.RULE_FIXED)
+    assert sel.n_keep == 3                          # clamped to K_k' = 3, not K_k = 4
+    for a in range(3):
+        assert 1 not in set(np.asarray(sel.kept[a]).tolist())
+    # with more iterations the kept (stale) centroid is what the next Step A sees, not a reseed
+    r3 = svoo.cocluster(Q, K, 3, 4, 3, init_q=init_q, init_k=init_k)
+    assert np.array_equal(r3.trace[2]["C_self"][1], K[11])
