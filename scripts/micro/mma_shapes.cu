@@ -11,6 +11,8 @@
 //           then PV pair (TS N=128, two accumulators interleaved, N/16 K-steps)
 //   mode 6: TS split by output columns: N=64 into O[:, 0:64] and O[:, 64:128] interleaved (one PV
 //           of a 128-wide head as two independent accumulators), 8 K-steps
+//   mode 7: SS at M = 64 (a half-height Q tile), K-steps of two accumulators interleaved
+//   mode 8: TS at M = 64 (P of a half-height tile from TMEM), two accumulators interleaved
 // ldw > 0: that many extra warps continuously tcgen05.ld their lanes' 64 S columns (the softmax
 // warps' TMEM reads competing with the MMAs' accumulator traffic)
 // The chain-free floor is 128 N / 256 = N / 2 cycles per instruction.
@@ -59,6 +61,14 @@ __global__ void __launch_bounds__(352, 1) k(long long* out, int iters, int n, in
             const uint32_t id64 = idesc_bf16(128, 64, 0, 1);
             mma_ts(tmem + 256, tmem + kk * 8, vd0 + vo, id64, 1);
             mma_ts(tmem + 320, tmem + kk * 8, vd0 + vo + (uint64_t)(8192 >> 4), id64, 1);
+          } else if (mode == 7) {
+            const uint32_t id64m = idesc_bf16(64, n, 0, 0);
+            mma_ss(tmem, ad0 + off, bd0 + off, id64m, 1);
+            mma_ss(tmem + 256, ad0 + off, bd0 + off, id64m, 1);
+          } else if (mode == 8) {
+            const uint32_t id64m = idesc_bf16(64, 128, 0, 1);
+            mma_ts(tmem + 256, tmem + kk * 8, vd0 + vo, id64m, 1);
+            mma_ts(tmem + 384, tmem + 128 + kk * 8, vd0 + vo, id64m, 1);
           } else if (mode == 4) {
             mma_ss(tmem, ad0 + off, bd0 + off, id_ss, 1);
             mma_ts(tmem + 256, tmem + 128 + kk * 8, vd0 + vo, id_ts, 1);
@@ -104,16 +114,16 @@ int main() {
   const int iters = 4000;
   const char* names[] = {"SS one acc", "SS two accs interleaved", "TS(N=128) one acc", "TS(N=128) two accs",
                          "SS + TS(N=128) interleaved", "attention step (QK2 + PV2)",
-                         "TS N=64 x2 (split O columns)"};
+                         "TS N=64 x2 (split O columns)", "SS M=64 two accs", "TS M=64 N=128 two accs"};
   for (int ldw = 0; ldw <= 8; ldw += 8)
-    for (int mode = 0; mode < 7; ++mode)
+    for (int mode = 0; mode < 9; ++mode)
       for (int n : {64, 80, 96, 128, 256}) {
-        if (((mode >= 2 && mode <= 3) || mode == 6) && n != 128) continue;
+        if (((mode >= 2 && mode <= 3) || mode == 6 || mode == 8) && n != 128) continue;
         if (mode == 5 && n > 128) continue;
         k<<<1, 352, 140000>>>(d, iters, n, mode, ldw);
         long long h = 0;
         cudaError_t e = cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
-        const int per_it = mode == 5 ? 16 + 2 * (n / 16) : ((mode == 1 || mode == 3 || mode == 4 || mode == 6) ? 16 : 8);
+        const int per_it = mode == 5 ? 16 + 2 * (n / 16) : ((mode == 1 || mode == 3 || mode == 4 || mode >= 6) ? 16 : 8);
         const double floor_c = mode == 5 ? (16 * n / 2 + 2 * (n / 16) * 64) / (double)per_it
                                          : (mode == 4 ? (n / 2 + 64) / 2.0 : (mode == 6 ? 32 : (mode >= 2 ? 64 : n / 2)));
         printf("ldw=%d %-28s N=%3d: %7.2f cycles per instruction (floor %.1f)%s %s\n", ldw, names[mode], n,
