@@ -11,13 +11,16 @@
 // Warp roles (352 threads):  warps 0-3 softmax/epilogue of Q tile 0 (TMEM lanes 0-127),
 // warps 4-7 the same for Q tile 1, warp 8 TMA producer (Q, K), warp 9 TMEM allocator + MMA
 // issuer, warp 10 TMA producer (V).
-// TMEM (512 cols): S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512); P (bf16x2) overwrites the
-// first 64 columns of its S buffer and feeds the PV MMA from TMEM (A operand), V from SMEM
-// (MN-major).  K and V have separate 2-slot rings: K(j) is released as soon as both QK(j) MMAs
-// complete and V(j) after both PV(j) MMAs, so each is prefetched ~2 tiles ahead.  MMA issue order
-// per KV tile j:  PV0(j), QK0(j+1), PV1(j), QK1(j+1) — the softmax of one Q tile overlaps the
-// MMAs of the other (FA4-style ping-pong).  Online softmax in the exp2 domain with lazy
-// rescaling (only when the running max grows by > 8, i.e. a factor 256).
+// TMEM (512 cols): S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512).  P (bf16x2) of keys 0-95
+// overwrites the first 48 columns of its S buffer and feeds the PV MMA from TMEM (A operand); P of
+// keys 96-127 goes to a per-set SMEM buffer (K-major SWIZZLE_64B) and feeds the last two PV K-steps
+// as SS MMAs; V from SMEM (MN-major).  K and V have separate 2-slot rings: K(j) is released as
+// soon as both QK(j) MMAs complete and V(j) after both PV(j), so each is prefetched ~2 tiles ahead.
+// MMA issue order per KV tile j:  PV0(j)[0-95], QK0(j+1), PV0(j)[96-127], PV1(j)[0-95], QK1(j+1),
+// PV1(j)[96-127] — the softmax of one Q tile overlaps the MMAs of the other (FA4-style
+// ping-pong), and QK(j+1) no longer waits for the exponentials of the last key quarter of tile j.
+// Online softmax in the exp2 domain with lazy rescaling (only when the running max grows by > 8,
+// i.e. a factor 256).
 // The inverse permutation is fused into the epilogue: row r of the tile is stored as 16-byte
 // vectors to O[b, h, perm_q[p], :] in original token order.
 #include "kernels.cuh"
@@ -72,9 +75,14 @@ struct Smem {
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_K = OFF_Q + 2 * QT;
   static constexpr int OFF_V = OFF_K + NST * KT;
-  static constexpr int OFF_BAR = OFF_V + NST * KT;
-  // q_full, k_full[2], k_empty[2], v_full[2], v_empty[2], s_full[2], p_full[2 tiles][2 halves], o_full
-  static constexpr int OFF_MISC = OFF_BAR + 16 * 8;  // tmem slot, R, n
+  // P of the last 32 keys of a tile, per accumulator set, K-major SWIZZLE_64B (128 rows x 64 B):
+  // the A operand of the two SS MMAs that finish PV(j) after QK(j+1) has been issued
+  static constexpr int PLT = BM * 64;
+  static constexpr int OFF_PL = OFF_V + NST * KT;
+  static constexpr int OFF_BAR = OFF_PL + 2 * PLT;
+  // q_full, k_full[2], k_empty[2], v_full[2], v_empty[2], s_full[2], p_full[2 sets][3 parts], o_full,
+  // pvd[2]
+  static constexpr int OFF_MISC = OFF_BAR + 24 * 8;  // tmem slot, R, n
   static constexpr int OFF_KSTART = OFF_MISC + 16;    // [n] first sorted row of kept cluster i
   static constexpr int OFF_RCUM = OFF_KSTART + kMaxClusters * 4;  // [n + 1] row prefix sums
   static constexpr int OFF_XCH = OFF_RCUM + ((kMaxClusters + 1) * 4 + 15) / 16 * 16;
@@ -102,8 +110,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint64_t* v_full = bars + 5;
   uint64_t* v_empty = bars + 7;
   uint64_t* s_full = bars + 9;
-  uint64_t* p_full = bars + 11;  // [tq * 2 + half]: P columns of keys [64 half, 64 half + 64)
-  uint64_t* o_full = bars + 15;
+  uint64_t* p_full = bars + 11;  // [tq * 3 + part]: P of keys 0-63 / 64-95 (TMEM), 96-127 (SMEM)
+  uint64_t* o_full = bars + 17;
+  uint64_t* pvd = bars + 18;     // [tq]: PV(j) of set tq complete (its SMEM part included)
   int* misc = reinterpret_cast<int*>(sm + L::OFF_MISC);
   int* kstart = reinterpret_cast<int*>(sm + L::OFF_KSTART);
   int* rcum = reinterpret_cast<int*>(sm + L::OFF_RCUM);
@@ -142,8 +151,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         mbar_init(v_full + s, 1); mbar_init(v_empty + s, 1);
       }
       for (int t = 0; t < 2; ++t) mbar_init(s_full + t, 1);
-      for (int t = 0; t < 4; ++t) mbar_init(p_full + t, 128);
+      for (int t = 0; t < 6; ++t) mbar_init(p_full + t, 128);
       mbar_init(o_full, 1);
+      for (int t = 0; t < 2; ++t) mbar_init(pvd + t, 1);
       fence_barrier_init();
       tma_prefetch_desc(&tm_q);
       const int ntq = has1 ? 2 : 1;
@@ -283,17 +293,28 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
       __syncwarp();
     };
-    // PV over the keys [64 half, 64 half + 64) of V slot `slot` (4 K-steps of 16 keys)
-    auto issue_pv = [&](int tq, int slot, int half, bool acc) {
+    // PV(j) in three parts: K-steps [k0, k1) with P from TMEM (keys 0-95, 6 K-steps), then keys
+    // 96-127 with P from SMEM (SS form, 2 K-steps) once QK(j+1) has been issued: QK(j+1) overwrites
+    // the TMEM columns of P, so it may only follow the TMEM parts of PV(j), and the last quarter of
+    // the exponentials no longer sits between S(j) and S(j+1).
+    auto issue_pv_tmem = [&](int tq, int slot, int k0, int k1, bool acc) {
       if (elect_one()) {
         const uint32_t d_tmem = tmem + 256 + tq * 128;
         const uint32_t p_tmem = tmem + tq * 128;
         const uint64_t vd = dv0 + (uint64_t)((slot * L::KT) >> 4);
-#pragma unroll
-        for (int k4 = 0; k4 < BN / 32; ++k4) {
-          const int kk2 = half * (BN / 32) + k4;
+        for (int kk2 = k0; kk2 < k1; ++kk2)
           mma_ts(d_tmem, p_tmem + kk2 * 8, vd + (uint64_t)((kk2 * 2048) >> 4), idesc_pv, (acc || kk2 > 0) ? 1u : 0u);
-        }
+      }
+      __syncwarp();
+    };
+    auto issue_pv_smem = [&](int tq, int slot) {
+      if (elect_one()) {
+        const uint32_t d_tmem = tmem + 256 + tq * 128;
+        const uint64_t pd = smem_desc_sw64(smem_u32(sm + L::OFF_PL + tq * L::PLT), 512);
+        const uint64_t vd = dv0 + (uint64_t)((slot * L::KT) >> 4);
+#pragma unroll
+        for (int kk2 = 6; kk2 < 8; ++kk2)
+          mma_ss(d_tmem, pd + (uint64_t)(((kk2 - 6) * 32) >> 4), vd + (uint64_t)((kk2 * 2048) >> 4), idesc_pv, 1u);
       }
       __syncwarp();
     };
@@ -301,13 +322,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       if (elect_one()) mma_commit(bar);
       __syncwarp();
     };
-    auto wait_pv = [&](int tq, int slot, int j) {
-      mbar_wait(p_full + tq * 2 + 0, j & 1);
+    auto pv_early = [&](int tq, int slot, int j) {
+      mbar_wait(p_full + tq * 3 + 0, j & 1);
       tc_fence_after();
-      issue_pv(tq, slot, 0, j > 0);
-      mbar_wait(p_full + tq * 2 + 1, j & 1);
+      issue_pv_tmem(tq, slot, 0, 4, j > 0);
+      mbar_wait(p_full + tq * 3 + 1, j & 1);
       tc_fence_after();
-      issue_pv(tq, slot, 1, true);
+      issue_pv_tmem(tq, slot, 4, 6, true);
+    };
+    auto pv_late = [&](int tq, int slot, int j) {
+      mbar_wait(p_full + tq * 3 + 2, j & 1);
+      tc_fence_after();
+      issue_pv_smem(tq, slot);
+      commit(pvd + tq);
     };
     
     mbar_wait(q_full, 0);
@@ -327,7 +354,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const bool more = j + 1 < nt;
         mbar_wait(v_full + slot, (j / NST) & 1);
         CS_TRACE(3, j);
-        wait_pv(0, slot, j);
+        pv_early(0, slot, j);
         CS_TRACE(4, j);
         if (more) {
           mbar_wait(k_full + slot1, ((j + 1) / NST) & 1);
@@ -336,15 +363,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           issue_qk(0, slot1, 0);
           commit(s_full + 0);
         }
+        pv_late(0, slot, j);
         if (has1) {
-          wait_pv(1, slot, j);
+          pv_early(1, slot, j);
           CS_TRACE(11, j);
+          if (more) { issue_qk(1, slot1, 1); commit(s_full + 1); }
+          pv_late(1, slot, j);
         }
         commit(v_empty + slot);
-        if (more) {
-          if (has1) { issue_qk(1, slot1, 1); commit(s_full + 1); }
-          commit(k_empty + slot1);
-        }
+        if (more) commit(k_empty + slot1);
       }
     } else {
       // split-KV: one Q tile (slot 0); accumulator set tq takes the KV tiles 2j + tq, which the
@@ -365,8 +392,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       for (int j = 0; 2 * j < nt; ++j) {
         const bool has_b = 2 * j + 1 < nt, more_a = 2 * j + 2 < nt, more_b = 2 * j + 3 < nt;
         mbar_wait(v_full + 0, j & 1);
-        wait_pv(0, 0, j);
-        commit(v_empty + 0);
+        pv_early(0, 0, j);
         if (more_a) {
           mbar_wait(k_full + 0, (j + 1) & 1);
           tc_fence_after();
@@ -374,10 +400,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           commit(s_full + 0);
           commit(k_empty + 0);
         }
+        pv_late(0, 0, j);
+        commit(v_empty + 0);
         if (has_b) {
           mbar_wait(v_full + 1, j & 1);
-          wait_pv(1, 1, j);
-          commit(v_empty + 1);
+          pv_early(1, 1, j);
           if (more_b) {
             mbar_wait(k_full + 1, (j + 1) & 1);
             tc_fence_after();
@@ -385,6 +412,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             commit(s_full + 1);
             commit(k_empty + 1);
           }
+          pv_late(1, 1, j);
+          commit(v_empty + 1);
         }
       }
     }
@@ -480,37 +509,61 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const float2 sl2 = make_float2(scale_log2, scale_log2), nm2 = make_float2(-m, -m);
         float2 acc4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
-        for (int hf = 0; hf < 2; ++hf) {
+        // exponentials of keys [c0, c1), packed in place over su[c0 / 2 ..): every kPolyEvery-th pair
+        // on the FMA pipe (polynomial), the rest on MUFU
+        auto exp_range = [&](int c0, int c1) {
 #pragma unroll
-          for (int c = hf * (BN / 2); c < (hf + 1) * (BN / 2); c += 2) {
+          for (int c = c0; c < c1; c += 2) {
             const float2 x = ffma2(make_float2(__uint_as_float(su[c]), __uint_as_float(su[c + 1])), sl2, nm2);
-            // every kPolyEvery-th pair on the FMA pipe (polynomial), the rest on MUFU: keeps
-            // MUFU below the tensor-core time of the two ping-ponged tiles
             const float2 p = (kPolyEvery > 0 && ((c >> 1) % kPolyEvery) == kPolyEvery - 1)
                                  ? ex2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
             acc4[(c >> 1) & 3] = fadd2(acc4[(c >> 1) & 3], p);
             su[c >> 1] = pack_bf16x2(p.x, p.y);
           }
-          tmem_st32(s_tm + hf * 32, su + hf * 32);
-          // lazy O rescale before PV(j) starts (it waits for p_full(j, half 0)).  tcgen05.ld/st
-          // are warp-collective, so the warp rescales if any of its rows needs it.  O is stable:
-          // PV(j-1) completed before s_full(j) (same commit order).
-          if (hf == 0 && warp_rescale) {
+        };
+        // part A: keys 0-63 -> TMEM columns 0-31
+        exp_range(0, 64);
+        tmem_st32(s_tm, su);
+        // lazy O rescale before PV(j) starts (it waits for p_full(j, part A)).  tcgen05.ld/st are
+        // warp-collective, so the warp rescales if any of its rows needs it.  O is stable once the
+        // SMEM part of PV(j-1) completed (pvd): the TMEM parts precede s_full(j) in commit order.
+        if (warp_rescale) {
+          if (j > 0) mbar_wait(pvd + tq, (j - 1) & 1);
+          tc_fence_after();
 #pragma unroll 1
-            for (int c = 0; c < D / 16; ++c) {
-              uint32_t ov[16];
-              tmem_ld16(o_tm + c * 16, ov);
-              tmem_wait_ld();
+          for (int c = 0; c < D / 16; ++c) {
+            uint32_t ov[16];
+            tmem_ld16(o_tm + c * 16, ov);
+            tmem_wait_ld();
 #pragma unroll
-              for (int i = 0; i < 16; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
-              tmem_st16(o_tm + c * 16, ov);
-            }
+            for (int i = 0; i < 16; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
+            tmem_st16(o_tm + c * 16, ov);
           }
-          tmem_wait_st();
-          tc_fence_before();
-          mbar_arrive(p_full + tq * 2 + hf);
-          if (hf == 0) CS_TRACE(14 + tq, j);
         }
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(p_full + tq * 3 + 0);
+        CS_TRACE(14 + tq, j);
+        // part B: keys 64-95 -> TMEM columns 32-47 (QK(j+1) follows its PV)
+        exp_range(64, 96);
+        tmem_st16(s_tm + 32, su + 32);
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(p_full + tq * 3 + 1);
+        // part C: keys 96-127 -> this set's SMEM P buffer (K-major SWIZZLE_64B: 16-byte chunk q of
+        // row r at chunk position q ^ ((r >> 1) & 3) of its 64-byte row, 8-row atoms of 512 B),
+        // once the SMEM part of PV(j-1) has read the previous contents
+        exp_range(96, 128);
+        if (j > 0) mbar_wait(pvd + tq, (j - 1) & 1);
+        {
+          uint8_t* prow = sm + Smem<D>::OFF_PL + tq * Smem<D>::PLT + (r >> 3) * 512 + (r & 7) * 64;
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            *reinterpret_cast<uint4*>(prow + ((q ^ ((r >> 1) & 3)) * 16)) =
+                make_uint4(su[48 + 4 * q], su[49 + 4 * q], su[50 + 4 * q], su[51 + 4 * q]);
+        }
+        fence_proxy_async_smem();
+        mbar_arrive(p_full + tq * 3 + 2);
         const float2 s01 = fadd2(acc4[0], acc4[1]), s23 = fadd2(acc4[2], acc4[3]);
         const float2 s4 = fadd2(s01, s23);
         l += s4.x + s4.y;

@@ -240,6 +240,17 @@ CS_DEV uint64_t smem_desc_sw128(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo
   desc |= (uint64_t)2 << 61;  // SWIZZLE_128B
   return desc;
 }
+// K-major SWIZZLE_64B canonical layout: rows of 64 B (32 bf16 along K), 8-row atoms of 512 B
+// (SBO = 512); a K = 16 step is a 32-byte start-address offset inside the row.
+CS_DEV uint64_t smem_desc_sw64(uint32_t saddr, uint32_t sbo_bytes) {
+  uint64_t desc = 0;
+  desc |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  desc |= (uint64_t)1 << 16;  // LBO (unused for swizzled K-major)
+  desc |= (uint64_t)((sbo_bytes >> 4) & 0x3FFFu) << 32;
+  desc |= (uint64_t)1 << 46;  // version
+  desc |= (uint64_t)4 << 61;  // SWIZZLE_64B
+  return desc;
+}
 // Instruction descriptor, kind::f16: bf16 A/B, fp32 D.  a_mn/b_mn = 1 for MN-major operands.
 __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, int a_mn, int b_mn) {
   return (1u << 4)                       // D format F32
