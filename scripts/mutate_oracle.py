@@ -37,6 +37,16 @@ MUTATIONS = [
     ("kept not re-sorted ascending", "kept = np.stack([np.sort(o[:n]) for o in orders])",
      "kept = np.stack([o[:n] for o in orders])"),
     ("n_b without the -1e-3 guard", "n = math.ceil(float(r) * Kk - 1e-3)", "n = math.ceil(float(r) * Kk)"),
+    ("attention scale sqrt(d) instead of 1/sqrt(d)", "scale = 1.0 / math.sqrt(d) if scale is None else scale",
+     "scale = math.sqrt(d) if scale is None else scale"),
+    ("attention over the query's own cluster label", "allowed = np.nonzero(np.isin(Lk, np.asarray(kept[a])))[0]",
+     "allowed = np.nonzero(Lk == a)[0]"),
+    ("counting sort scatter in reverse (unstable)", "    for i, c in enumerate(labels):\n        perm[pos[int(c)]] = i",
+     "    for i, c in reversed(list(enumerate(labels))):\n        perm[pos[int(c)]] = i"),
+    ("centroid mean over all tokens of the side", "C[j] = members.sum(axis=0) / members.shape[0]",
+     "C[j] = members.sum(axis=0) / X.shape[0]"),
+    ("n clamped to K_k instead of K_k'", "return int(min(max(n, 1), Kk_ne))", "return int(min(max(n, 1), Kk))"),
+    ("Floyd inserts t on a collision", "chosen.add(j if t in chosen else t)", "chosen.add(t)"),
 ]
 
 
