@@ -304,6 +304,15 @@ cs_status coclust_sparse_attention_ulysses(int H, int N, int d, cs_bf16_in q, cs
 cs_status cs_ulysses_pack(int Nl, int P, int Hl, int d, int T, const void* const* srcs, void* dst,
                           void* stream);
 
+/* Head-group form of cs_ulysses_pack (the in-bound exchange split by head groups, so
+ * group g+1's all_to_all overlaps group g's layer): packs only heads [g*Hg, (g+1)*Hg) of every
+ * rank's Hl-head block, dst [P, Nl, T, Hg, d]; after the all_to_all_single tensor t is the
+ * [1, Hg, N, d] view with strides (d, T*Hg*d) of the receive buffer.  Hg must divide Hl,
+ * 0 <= g < Hl/Hg; cs_ulysses_pack is the case Hg = Hl, g = 0.  Same pointer rules; CS_ERR_ARG on a
+ * bad group. */
+cs_status cs_ulysses_pack_group(int Nl, int P, int Hl, int Hg, int g, int d, int T, const void* const* srcs,
+                                void* dst, void* stream);
+
 /* Device-side barrier over P ranks: peer_flags = DEVICE array of P uint64 pointers to every
  * rank's int32 flag array [P] (zero-initialised, mapped here); rank `rank` writes `epoch` into
  * flags_p[rank] of every rank p (system-scope release) after all earlier work on `stream`, then

@@ -81,6 +81,7 @@ _SIG = {
                                               _I, _I, _P, ctypes.c_double, ctypes.c_double, _I, _I, ctypes.c_float,
                                               _BF16Out, _P, _P, _P, ctypes.c_size_t, _P, _P]),
     "cs_ulysses_pack": (_I, [_I, _I, _I, _I, _I, _P, _P, _P]),
+    "cs_ulysses_pack_group": (_I, [_I, _I, _I, _I, _I, _I, _I, _P, _P, _P]),
     "cs_ipc_handle": (_I, [_P, _P, ctypes.POINTER(ctypes.c_size_t)]),
     "cs_ipc_open": (_I, [_P, ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)]),
     "cs_ipc_close": (_I, [_P, ctypes.c_size_t]),
@@ -388,9 +389,10 @@ def coclust_sparse_attention_ulysses(q, k, v, kq, kk, iters, budget, *, out=None
     return out
 
 
-def ulysses_pack(blocks, P, out=None):
-    """T rank-local token blocks [1, Nl, P*Hl, d] (bf16, contiguous) -> [P, Nl, T, Hl, d] (one send
-    buffer for a single all_to_all_single of all T tensors)."""
+def ulysses_pack(blocks, P, out=None, groups=1, group=0):
+    """T rank-local token blocks [1, Nl, P*Hl, d] (bf16, contiguous) -> [P, Nl, T, Hg, d] (one send
+    buffer for a single all_to_all_single of all T tensors); Hg = Hl / groups: only the heads
+    [group Hg, (group+1) Hg) of every rank's Hl-head block (groups = 1: all of them)."""
     x0 = blocks[0]
     _cuda(x0, "blocks[0]")
     _, Nl, H, d = x0.shape
@@ -398,12 +400,15 @@ def ulysses_pack(blocks, P, out=None):
     if H % P:
         raise ValueError("H must be divisible by P")
     Hl = H // P
+    if groups < 1 or Hl % groups or not 0 <= group < groups:
+        raise ValueError("groups must divide H / P and 0 <= group < groups")
+    Hg = Hl // groups
     for b in blocks:
         if b.shape != x0.shape or not b.is_contiguous() or b.dtype != torch.bfloat16:
             raise ValueError("blocks must be contiguous bf16 tensors of one shape")
-    out = torch.empty(P, Nl, T, Hl, d, dtype=torch.bfloat16, device=x0.device) if out is None else out
+    out = torch.empty(P, Nl, T, Hg, d, dtype=torch.bfloat16, device=x0.device) if out is None else out
     srcs = (ctypes.c_void_p * T)(*[b.data_ptr() for b in blocks])
-    _check(lib().cs_ulysses_pack(Nl, P, Hl, d, T, srcs, _ptr(out), _stream(x0)))
+    _check(lib().cs_ulysses_pack_group(Nl, P, Hl, Hg, group, d, T, srcs, _ptr(out), _stream(x0)))
     return out
 
 

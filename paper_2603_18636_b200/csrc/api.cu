@@ -750,9 +750,12 @@ cs_status coclust_sparse_attention_ulysses(int H, int N, int d, cs_bf16_in q, cs
                    flags, scale, out, s, true, c, static_cast<cudaStream_t>(stream), stage_events, peer, v_ready);
 }
 
-cs_status cs_ulysses_pack(int Nl, int P, int Hl, int d, int T, const void* const* srcs, void* dst, void* stream) {
+cs_status cs_ulysses_pack_group(int Nl, int P, int Hl, int Hg, int g, int d, int T, const void* const* srcs,
+                                void* dst, void* stream) {
   g_err[0] = 0;
   if (Nl <= 0 || P <= 0 || Hl <= 0 || (d != 64 && d != 128)) return fail(CS_ERR_SHAPE, "Nl, P, Hl > 0, d in {64, 128}");
+  if (Hg <= 0 || Hl % Hg || g < 0 || g >= Hl / Hg)
+    return fail(CS_ERR_ARG, "need Hg > 0 dividing Hl and 0 <= g < Hl / Hg (Hl %d, Hg %d, g %d)", Hl, Hg, g);
   if (T < 1 || T > 4) return fail(CS_ERR_ARG, "T must be in [1, 4] (got %d)", T);
   NEED(srcs, "srcs"); NEED(dst, "dst");
   UlyssesSrcs u{};
@@ -762,8 +765,14 @@ cs_status cs_ulysses_pack(int Nl, int P, int Hl, int d, int T, const void* const
     u.p[t] = static_cast<const uint4*>(srcs[t]);
   }
   if (reinterpret_cast<uintptr_t>(dst) % 16) return fail(CS_ERR_ALIGN, "dst not 16-byte aligned");
-  CS_CUDA(launch_ulysses_pack(Nl, P, T, (size_t)Hl * d * 2, u, dst, static_cast<cudaStream_t>(stream)), "ulysses_pack");
+  CS_CUDA(launch_ulysses_pack(Nl, P, T, (size_t)Hg * d * 2, (size_t)Hl * d * 2, (size_t)g * Hg * d * 2, u, dst,
+                              static_cast<cudaStream_t>(stream)),
+          "ulysses_pack");
   return CS_OK;
+}
+
+cs_status cs_ulysses_pack(int Nl, int P, int Hl, int d, int T, const void* const* srcs, void* dst, void* stream) {
+  return cs_ulysses_pack_group(Nl, P, Hl, Hl, 0, d, T, srcs, dst, stream);
 }
 
 cs_status cs_peer_barrier(int P, int rank, const void* peer_flags, int epoch, void* stream) {

@@ -715,11 +715,14 @@ cudaError_t launch_block_transpose(int A, int B, size_t row_bytes, const void* s
 }
 
 // Ulysses in-bound pack (a13): T token blocks src_t [Nl, P * Hl, d] (rank-local tokens, all heads)
-// -> dst [P, Nl, T, Hl, d]: chunk p (the heads of rank p) holds, per token, the T tensors' head
-// rows side by side, so after ONE all_to_all_single the receiver sees [N, T, Hl, d] and tensor t
-// is the strided [Hl, N, d] view (token stride T Hl d) the layer reads without a copy.
-__global__ void __launch_bounds__(256) k_ulysses_pack(int Nl, int P, int T, int vpr, UlyssesSrcs srcs,
-                                                      uint4* __restrict__ dst) {
+// -> dst [P, Nl, T, Hg, d] for the head group g (heads [g Hg, (g+1) Hg) of every rank's Hl-head
+// block; Hg = Hl: all of them): chunk p (destination rank p) holds, per token, the T tensors' head
+// rows side by side, so after ONE all_to_all_single the receiver sees [N, T, Hg, d] and tensor t is
+// the strided [Hg, N, d] view (token stride T Hg d) the layer reads without a copy.
+// vpr = 16-byte vectors per packed row (Hg d bf16), sstride / soff = vectors between consecutive
+// (token, rank) rows of a source and the group's offset in such a row.
+__global__ void __launch_bounds__(256) k_ulysses_pack(int Nl, int P, int T, int vpr, int sstride, int soff,
+                                                      UlyssesSrcs srcs, uint4* __restrict__ dst) {
   const long long total = (long long)P * Nl * T * vpr;
   for (long long i = blockIdx.x * 256LL + threadIdx.x; i < total; i += (long long)gridDim.x * 256) {
     const int v = (int)(i % vpr);
@@ -727,17 +730,18 @@ __global__ void __launch_bounds__(256) k_ulysses_pack(int Nl, int P, int T, int 
     const int t = (int)(r % T);
     r /= T;
     const int n = (int)(r % Nl), p = (int)(r / Nl);
-    dst[i] = srcs.p[t][((long long)n * P + p) * vpr + v];
+    dst[i] = srcs.p[t][((long long)n * P + p) * sstride + soff + v];
   }
 }
 
-cudaError_t launch_ulysses_pack(int Nl, int P, int T, size_t row_bytes, const UlyssesSrcs& srcs, void* dst,
-                                cudaStream_t st) {
+cudaError_t launch_ulysses_pack(int Nl, int P, int T, size_t row_bytes, size_t src_row_bytes, size_t src_off_bytes,
+                                const UlyssesSrcs& srcs, void* dst, cudaStream_t st) {
   const int vpr = (int)(row_bytes / 16);
   const long long total = (long long)P * Nl * T * vpr;
   const long long want = (total + 255) / 256;
   const int grid = (int)(want < 148 * 16 ? want : 148 * 16);
-  k_ulysses_pack<<<grid > 0 ? grid : 1, 256, 0, st>>>(Nl, P, T, vpr, srcs, static_cast<uint4*>(dst));
+  k_ulysses_pack<<<grid > 0 ? grid : 1, 256, 0, st>>>(Nl, P, T, vpr, (int)(src_row_bytes / 16),
+                                                      (int)(src_off_bytes / 16), srcs, static_cast<uint4*>(dst));
   return cudaGetLastError();
 }
 }  // namespace cs

@@ -43,8 +43,8 @@ cudaError_t launch_block_transpose(int A, int B, size_t row_bytes, const void* s
 struct UlyssesSrcs {
   const uint4* p[4];
 };
-cudaError_t launch_ulysses_pack(int Nl, int P, int T, size_t row_bytes, const UlyssesSrcs& srcs, void* dst,
-                                cudaStream_t st);
+cudaError_t launch_ulysses_pack(int Nl, int P, int T, size_t row_bytes, size_t src_row_bytes, size_t src_off_bytes,
+                                const UlyssesSrcs& srcs, void* dst, cudaStream_t st);
 cudaError_t launch_permute_rows(XView x, int BH, int N, int d, const int32_t* perm,
                                 __nv_bfloat16* xp, cudaStream_t st);
 

@@ -48,9 +48,9 @@ class CudaOps:
     pack, the layer entry, the out-bound unpack, the device barrier, and the side stream V's
     exchange runs on.  The CPU tests substitute a reference implementation of the same contract."""
 
-    def pack(self, blocks, P):
+    def pack(self, blocks, P, groups=1, group=0):
         import paper_2603_18636_b200 as pb
-        return pb.ulysses_pack(blocks, P)
+        return pb.ulysses_pack(blocks, P, groups=groups, group=group)
 
     def transpose(self, x, A, B):
         import paper_2603_18636_b200 as pb
@@ -79,9 +79,32 @@ class CudaOps:
         send.record_stream(side)
         return recv, ev
 
+    def exchange_chain(self, sends, a2a):
+        """The all-to-alls of `sends`, in order, on ONE side stream ordered after the current stream
+        (one communicator, one issue order on every rank); -> [(recv, event)] per send."""
+        import torch
+        cur = torch.cuda.current_stream(sends[0].device)
+        side = torch.cuda.Stream(sends[0].device)
+        side.wait_stream(cur)
+        res = []
+        with torch.cuda.stream(side):
+            for send in sends:
+                recv = torch.empty_like(send)
+                a2a(recv, send)
+                ev = torch.cuda.Event()
+                ev.record(side)
+                recv.record_stream(cur)
+                send.record_stream(side)
+                res.append((recv, ev))
+        return res
+
+    def wait(self, ev):
+        import torch
+        torch.cuda.current_stream().wait_event(ev)
+
 
 def ulysses_layer(q_loc, k_loc, v_loc, kq, kk, iters, budget, *, group=None, a2a=None, peer=None,
-                  overlap_v=False, ops=None, **kw):
+                  overlap_v=False, head_groups=1, ops=None, **kw):
     """Sequence-parallel SVOO layer.
 
     q_loc, k_loc, v_loc: [1, N/P, H, d] bf16 token blocks of this rank (rank r holds tokens
@@ -95,6 +118,11 @@ def ulysses_layer(q_loc, k_loc, v_loc, kq, kk, iters, budget, *, group=None, a2a
     just before the V permute (coclust_sparse_attention_ulysses, v_ready).  On one GPU (P = 1,
     where the exchange is a local copy) that variant is erratic (occasional +10-14 ms layers) and
     not faster, so it is opt-in; its value on an NVLink box is unmeasured.
+    head_groups=G > 1 splits the in-bound exchange by head groups instead: G packed
+    Q|K|V buffers (cs_ulysses_pack_group, heads [g Hl/G, (g+1) Hl/G) of every rank's block), their
+    all_to_alls in order on one side stream, and the layer of group g (its own call, global head
+    offset r Hl + g Hl/G) waits only for exchange g — exchange g+1 overlaps layer g.  Each head's
+    result is bit-identical to the single-call layer (per-head work, global sampler streams).
     Out-bound: `peer` (a PeerOutput) -> the attention epilogue stores every row straight into the
     owning rank's token block (fused return, then a device barrier); else one all_to_all_single of
     O + unpack.  `a2a(recv, send)` overrides the exchange (e.g. through host memory for a gloo
@@ -112,6 +140,35 @@ def ulysses_layer(q_loc, k_loc, v_loc, kq, kk, iters, budget, *, group=None, a2a
     N = Nl * P
     a2a = a2a or (lambda recv, send: dist.all_to_all_single(recv, send, group=group))
     blocks = [x.contiguous() for x in (q_loc, k_loc, v_loc)]
+    kw.setdefault("heads_total", H)
+    if head_groups > 1:
+        if overlap_v or Hl % head_groups:
+            raise ValueError("head_groups must divide H / P and excludes overlap_v")
+        G, Hg = head_groups, Hl // head_groups
+        base = kw.pop("head_offset", r * Hl)
+        exch = ops.exchange_chain([ops.pack(blocks, P, groups=G, group=g) for g in range(G)], a2a)
+        if peer is None:
+            out_buf = torch.empty(N, Hl, d, dtype=q_loc.dtype, device=q_loc.device)
+            o_view = out_buf.permute(1, 0, 2).unsqueeze(0)
+        for g, (rg, ev) in enumerate(exch):
+            if ev is not None:
+                ops.wait(ev)
+            gv = lambda t: rg.view(N, 3, Hg, d)[:, t].permute(1, 0, 2).unsqueeze(0)
+            bud = budget[r * Hl + g * Hg:r * Hl + (g + 1) * Hg].contiguous()
+            if peer is not None:
+                ops.layer(gv(0), gv(1), gv(2), kq, kk, iters, bud, head_offset=base + g * Hg,
+                          peer=dict(ptrs=peer.ptrs, P=P, n_per_rank=Nl, head_base=r * Hl + g * Hg, s_tok=H * d,
+                                    s_head=d), **kw)
+            else:
+                ops.layer(gv(0), gv(1), gv(2), kq, kk, iters, bud, head_offset=base + g * Hg,
+                          out=o_view[:, g * Hg:(g + 1) * Hg], **kw)
+        if peer is not None:
+            peer.epoch += 1
+            ops.barrier(peer, P, r, q_loc)
+            return peer.out
+        back = torch.empty_like(out_buf)
+        a2a(back.view(P, Nl * Hl * d), out_buf.view(P, Nl * Hl * d))
+        return ops.transpose(back.view(P, Nl * Hl * d), P, Nl).view(1, Nl, H, d)
     v_ready = None
     if overlap_v:
         send_qk = ops.pack(blocks[:2], P)                        # [P, Nl, 2, Hl, d]
@@ -130,7 +187,6 @@ def ulysses_layer(q_loc, k_loc, v_loc, kq, kk, iters, budget, *, group=None, a2a
     # [N, T, Hl, d] receive buffer: tensor t is the [1, Hl, N, d] view with strides (d, T Hl d)
     view = lambda t: qk_buf.view(N, T_qk, Hl, d)[:, t].permute(1, 0, 2).unsqueeze(0)
     kw.setdefault("head_offset", r * Hl)
-    kw.setdefault("heads_total", H)
     bud = budget[r * Hl:(r + 1) * Hl].contiguous()
     if peer is not None:
         ops.layer(view(0), view(1), v_view, kq, kk, iters, bud, v_ready=v_ready,

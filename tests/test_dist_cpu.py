@@ -83,9 +83,11 @@ class _CpuOps:
     with the same contracts, so the host logic (pack layout, strided views, head offsets, the two
     exchanges, unpack) runs under gloo on CPU."""
 
-    def pack(self, blocks, P):  # cs_ulysses_pack: [1, Nl, P*Hl, d] x T -> [P, Nl, T, Hl, d]
+    def pack(self, blocks, P, groups=1, group=0):  # cs_ulysses_pack(_group): -> [P, Nl, T, Hg, d]
         _, Nl, H, d = blocks[0].shape
-        st = torch.stack([b[0].reshape(Nl, P, H // P, d) for b in blocks], dim=2)   # [Nl, P, T, Hl, d]
+        Hg = H // P // groups
+        st = torch.stack([b[0].reshape(Nl, P, H // P, d)[:, :, group * Hg:(group + 1) * Hg] for b in blocks],
+                         dim=2)                                                   # [Nl, P, T, Hg, d]
         return st.permute(1, 0, 2, 3, 4).contiguous()
 
     def transpose(self, x, A, B):  # cs_block_transpose
@@ -108,8 +110,14 @@ class _CpuOps:
         a2a(recv, send)
         return recv, None
 
+    def exchange_chain(self, sends, a2a):
+        return [self.exchange_async(s_, a2a) for s_ in sends]
 
-def _ulysses_worker(rank, world, port, overlap_v, ret):
+    def wait(self, ev):
+        pass
+
+
+def _ulysses_worker(rank, world, port, overlap_v, ret, head_groups=1):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2603_18636_b200.dist import ulysses_layer
@@ -119,7 +127,8 @@ def _ulysses_worker(rank, world, port, overlap_v, ret):
     Nl = N // world
     blk = lambda t: t[0].permute(1, 0, 2)[rank * Nl:(rank + 1) * Nl].unsqueeze(0).double().contiguous()
     budget = torch.tensor([0.3, 0.2, 0.5, 0.25])
-    o = ulysses_layer(blk(w.q), blk(w.k), blk(w.v), 6, 10, 2, budget, ops=_CpuOps(), overlap_v=overlap_v)
+    o = ulysses_layer(blk(w.q), blk(w.k), blk(w.v), 6, 10, 2, budget, ops=_CpuOps(), overlap_v=overlap_v,
+                      head_groups=head_groups)
     gathered = [None] * world
     dist.all_gather_object(gathered, (rank, o.numpy()))
     if rank == 0:
@@ -128,8 +137,8 @@ def _ulysses_worker(rank, world, port, overlap_v, ret):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("overlap_v", [True, False])
-def test_two_rank_ulysses_matches_single_process(overlap_v):
+@pytest.mark.parametrize("overlap_v,head_groups", [(True, 1), (False, 1), (False, 2)])
+def test_two_rank_ulysses_matches_single_process(overlap_v, head_groups):
     """Sequence-sharded inputs -> packed Q|K all-to-all (+ V's own, or one packed Q|K|V) -> per-head
     layer on the strided receive views -> all-to-all back + unpack == the layer run on the whole
     sequence in one process (same per-head sampler streams)."""
@@ -139,7 +148,8 @@ def test_two_rank_ulysses_matches_single_process(overlap_v):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_ulysses_worker, args=(r, world, port, overlap_v, q)) for r in range(world)]
+    procs = [ctx.Process(target=_ulysses_worker, args=(r, world, port, overlap_v, q, head_groups))
+             for r in range(world)]
     for p in procs:
         p.start()
     got = q.get(timeout=300)          # [1, N, H, d]
@@ -168,3 +178,16 @@ def test_ulysses_pack_layout_reference():
         recv = torch.cat([sends[src][dst] for src in range(P)])          # [N, T, Hl, d] (source-major)
         for t in range(T):
             assert torch.equal(recv[:, t], full[t][0, :, dst * Hl:(dst + 1) * Hl])
+
+
+def test_ulysses_pack_group_layout_reference():
+    """cs_ulysses_pack_group's contract: group g of G exchanges heads [g Hg, (g+1) Hg) of every
+    rank's Hl-head block; the G receive buffers together hold exactly the single-pack buffer."""
+    P, Nl, Hl, d, T, G = 2, 3, 4, 8, 3, 2
+    H, Hg = P * Hl, Hl // G
+    x = [torch.randn(1, Nl, H, d, dtype=torch.float64) for _ in range(T)]
+    ops = _CpuOps()
+    whole = ops.pack(x, P)                                       # [P, Nl, T, Hl, d]
+    for g in range(G):
+        part = ops.pack(x, P, groups=G, group=g)                 # [P, Nl, T, Hg, d]
+        assert torch.equal(part, whole[:, :, :, g * Hg:(g + 1) * Hg])

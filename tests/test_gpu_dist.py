@@ -79,6 +79,46 @@ def test_ulysses_pack_kernel_matches_reference():
         assert torch.equal(got, ref)
 
 
+def test_ulysses_pack_group_kernel_matches_reference():
+    """cs_ulysses_pack_group: group g of G holds heads [g Hg, (g+1) Hg) of every rank's block."""
+    import paper_2603_18636_b200 as pb
+    P, Nl, H, d, T = 2, 29, 8, 128, 3
+    blocks = [torch.randn(1, Nl, H, d, device="cuda").to(torch.bfloat16) for _ in range(T)]
+    whole = pb.ulysses_pack(blocks, P)                                   # [P, Nl, T, Hl, d]
+    for G in (2, 4):
+        Hg = H // P // G
+        for g in range(G):
+            assert torch.equal(pb.ulysses_pack(blocks, P, groups=G, group=g), whole[:, :, :, g * Hg:(g + 1) * Hg])
+    with pytest.raises(ValueError):
+        pb.ulysses_pack(blocks, P, groups=3)
+
+
+def test_ulysses_head_groups_single_rank_equals_layer():
+    """Exchange split by head groups (one all-to-all per group on a side stream, the layer of group
+    g after exchange g): P = 1 over NCCL, G = 2 and 4, bit-equal to the single-call layer; and the
+    fused return path with G = 2."""
+    import torch.distributed as dist
+    import paper_2603_18636_b200 as pb
+    from paper_2603_18636_b200.dist import PeerOutput, ulysses_layer
+    from synthetic import video_qkv
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{_port()}", rank=0, world_size=1)
+    w = video_qkv(4, 16, 24, 4, 128, seed=6, device="cuda")
+    budget = torch.tensor([0.2, 0.3, 0.25, 0.4], device="cuda")
+    ref = pb.coclust_sparse_attention(w.q, w.k, w.v, 24, 64, 2, budget)
+    tok = lambda t: t.permute(0, 2, 1, 3).contiguous()
+    for G in (2, 4):
+        o = ulysses_layer(tok(w.q), tok(w.k), tok(w.v), 24, 64, 2, budget, head_groups=G)
+        torch.cuda.synchronize()
+        assert torch.equal(o, tok(ref)), G
+    peer = PeerOutput(w.q.shape[2], 4, 128, "cuda")
+    o = ulysses_layer(tok(w.q), tok(w.k), tok(w.v), 24, 64, 2, budget, head_groups=2, peer=peer)
+    torch.cuda.synchronize()
+    assert torch.equal(o, tok(ref))
+    peer.close()
+    dist.destroy_process_group()
+
+
 def _oracle_check(w, o_tok, budget, rows=256):
     """o_tok [1, N, H, d] (token layout) vs the oracle's masked attention on the single-process
     partition (the GPU's labels / kept blocks, bit-identical to the sharded run's), sampled rows."""
