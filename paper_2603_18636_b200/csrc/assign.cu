@@ -395,7 +395,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         asg::argmax_chunk<BIAS>(tmem + lane_off + buf * NCH_MAX, nch, c * nch, ks, bias_row, best, best_j, keep);
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(acc_empty + buf), 0));
+        // relaxed: the TMEM reads are complete (tcgen05.wait::ld), nothing in memory to publish; a
+        // release arrive at cluster scope costs a memory barrier per chunk (ncu: ERRBAR, 13 % of
+        // the kernel's stall samples)
+        if (lane == 0) {
+#ifdef CS_ARRIVE_RELEASE
+          mbar_arrive_cluster(mapa_shared(smem_u32(acc_empty + buf), 0));
+#else
+          mbar_arrive_cluster_relaxed(mapa_shared(smem_u32(acc_empty + buf), 0));
+#endif
+        }
       }
       best_j = asg::argmax_finish(best, best_j, keep);
       const int n = n0 + (int)rank * BM + r;

@@ -147,6 +147,11 @@ CS_DEV uint32_t mapa_shared(uint32_t saddr, uint32_t rank) {
 CS_DEV void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+// Relaxed remote arrive: no release fence (the arriving threads publish no generic-memory writes;
+// their tcgen05.ld reads of TMEM are complete after tcgen05.wait::ld)
+CS_DEV void mbar_arrive_cluster_relaxed(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
 CS_DEV void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
