@@ -385,8 +385,9 @@ cudaError_t launch_kmeans_prep(const float* cself, int ks, int ks_pad, int BH, i
 }
 
 // ---------------------------------------------------------------------------------------------
-// a5/a7: centroid update.  grid (ceil(K / CPB), BH), block 256 (8 warps), CPB = 8 / NWC clusters
-// per CTA with NWC warps each (NWC from the mean cluster size, so small clusters do not leave
+// a5/a7: centroid update.  grid (ceil(K / CPB), BH), block 32 NWC CPB threads: CPB clusters per
+// CTA (1 by default: a CTA's warps never wait at the final barrier for a larger cluster sharing
+// the CTA) with NWC warps each (NWC from the mean cluster size, so small clusters do not leave
 // most of a CTA idle).  Warp ws of a cluster sums a contiguous chunk of its sorted positions;
 // fixed order -> deterministic.  Empty cluster: untouched (R5).
 // ---------------------------------------------------------------------------------------------
@@ -401,10 +402,10 @@ __global__ void __launch_bounds__(256) k_seg_mean(XView x, int N, int K, int nwc
 #ifndef CS_SEG_U
 #define CS_SEG_U 8
 #endif
-  constexpr int NW = 8, U = CS_SEG_U;  // warps, rows in flight per lane group
-  __shared__ float part[NW * RPW][D];
+  constexpr int NWMAX = 8, U = CS_SEG_U;  // warps (at most), rows in flight per lane group
+  __shared__ float part[NWMAX * RPW][D];
   const int bh = blockIdx.y;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, NW = blockDim.x >> 5;
   const int cpb = NW / nwc, cl = w / nwc, ws = w % nwc;
   const int j = blockIdx.x * cpb + cl;
   const int grp = lane / LPR, gl = lane % LPR;  // row group inside the warp, lane inside the row
@@ -440,7 +441,7 @@ __global__ void __launch_bounds__(256) k_seg_mean(XView x, int N, int K, int nwc
   for (int i = 0; i < 8; ++i) part[w * RPW + grp][gl * 8 + i] = acc[i];
   __syncthreads();
   // cluster c of the CTA: partial rows [c nwc RPW, (c+1) nwc RPW), summed in a fixed order
-  for (int o = threadIdx.x; o < cpb * D; o += 256) {
+  for (int o = threadIdx.x; o < cpb * D; o += blockDim.x) {
     const int c = o / D, col = o % D, jc = blockIdx.x * cpb + c;
     if (jc >= K) continue;
     const int n = of[jc + 1] - of[jc];
@@ -662,11 +663,16 @@ cudaError_t launch_seg_mean(XView x, int BH, int N, int d, int K, const int32_t*
   const int mean = N / K;
   int nwc = 1;
   while (nwc < 8 && nwc * CS_SEG_ROWS < mean) nwc <<= 1;
-  const dim3 grid((K + 8 / nwc - 1) / (8 / nwc), BH);
+#ifndef CS_SEG_CPB
+#define CS_SEG_CPB 1  // clusters per CTA: one, so a CTA's warps never wait for another cluster's rows
+#endif
+  const int cpb = CS_SEG_CPB * nwc > 8 ? 8 / nwc : CS_SEG_CPB;
+  const dim3 grid((K + cpb - 1) / cpb, BH);
+  const int threads = 32 * nwc * cpb;
   if (d == 128)
-    k_seg_mean<128><<<grid, 256, 0, st>>>(x, N, K, nwc, perm, offs, C, xperm);
+    k_seg_mean<128><<<grid, threads, 0, st>>>(x, N, K, nwc, perm, offs, C, xperm);
   else
-    k_seg_mean<64><<<grid, 256, 0, st>>>(x, N, K, nwc, perm, offs, C, xperm);
+    k_seg_mean<64><<<grid, threads, 0, st>>>(x, N, K, nwc, perm, offs, C, xperm);
   return cudaGetLastError();
 }
 
