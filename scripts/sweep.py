@@ -128,32 +128,34 @@ def run_cells(a):
 
 
 def run_heads(a):
-    """Head-parallel scaling on one GPU: the layer of rank 0 at P = 1, 2, 4, 8 (its H / P heads,
+    """Head-parallel scaling on one GPU: every rank's layer at P = 1, 2, 4, 8 (its H / P heads,
     global sampler keys), i.e. the per-rank work of BASELINE configs[2] without the other ranks.
     Head-parallel has no collective on the data path, so the P-GPU layer time is the max over
-    ranks of these per-rank times (ranks differ only by their heads' budgets / cluster sizes)."""
+    ranks of these per-rank times (ranks differ only by their heads' budgets / cluster sizes).
+    The (P, rank) layers are captured once (CUDA graphs over head views of one tensor) and timed
+    in `--rounds` interleaved rounds; each (P, rank) reports its median over the rounds, so clock
+    drift over the run (power capping) does not bias the ranks measured first or last."""
+    import statistics
     dev = torch.device("cuda", 0)
     c = CONFIGS["wan14b_720p"]
     w = video_qkv(c["T"], c["Hs"], c["Ws"], c["H"], c["d"], seed=a.seed, device=dev)
     H = c["H"]
     ws = pb.Workspace()
-    rows = []
-    fout = open(a.out, "w") if a.out else None
-    base = None
-    for P in (1, 2, 4, 8):
+    Ps = (1, 2, 4, 8)
+    calls = {}
+    for P in Ps:
         Hl = H // P
-        times = []
         for r in range(P) if a.all_ranks else range(1):
             sl = slice(r * Hl, (r + 1) * Hl)
-            q, k, v = (t[:, sl].contiguous() for t in (w.q, w.k, w.v))
-            out = torch.empty_like(q)
+            q, k, v = (t[:, sl] for t in (w.q, w.k, w.v))  # head views, no copy
+            out = torch.empty(1, Hl, w.q.shape[2], c["d"], dtype=w.q.dtype, device=dev)
             budget = torch.full((Hl,), 0.2, dtype=torch.float32, device=dev)
+            call = (lambda q=q, k=k, v=v, out=out, budget=budget, r=r, Hl=Hl:
+                    pb.coclust_sparse_attention(q, k, v, c["kq"], c["kk"], c["iters"], budget, seed=a.seed,
+                                                rule=RULES["fixed"], out=out, ws=ws, head_offset=r * Hl,
+                                                heads_total=H))
             for _ in range(a.warmup):
-                pb.coclust_sparse_attention(q, k, v, c["kq"], c["kk"], c["iters"], budget, seed=a.seed,
-                                            rule=RULES["fixed"], out=out, ws=ws, head_offset=r * Hl, heads_total=H)
-            call = lambda: pb.coclust_sparse_attention(q, k, v, c["kq"], c["kk"], c["iters"], budget, seed=a.seed,
-                                                       rule=RULES["fixed"], out=out, ws=ws, head_offset=r * Hl,
-                                                       heads_total=H)
+                call()
             if a.graph:
                 torch.cuda.synchronize()
                 g = torch.cuda.CUDAGraph()
@@ -161,24 +163,35 @@ def run_heads(a):
                     call()
                 call = g.replay
                 call()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            calls[(P, r)] = call
+    samples = {key: [] for key in calls}
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for rnd in range(a.rounds):
+        keys = list(calls)
+        if rnd % 2:
+            keys.reverse()
+        for key in keys:
+            call = calls[key]
             torch.cuda.synchronize()
             e0.record()
             for _ in range(a.steps):
                 call()
             e1.record()
             torch.cuda.synchronize()
-            times.append(e0.elapsed_time(e1) / a.steps)
-            del q, k, v, out
+            samples[key].append(e0.elapsed_time(e1) / a.steps)
+    rows = []
+    fout = open(a.out, "w") if a.out else None
+    base = None
+    for P in Ps:
+        times = [statistics.median(samples[(P, r)]) for r in range(P) if (P, r) in samples]
         t = max(times)
         base = base or t
-        row = {"P": P, "heads_per_rank": Hl, "ms_per_rank_max": t, "ms_per_rank": times,
-               "predicted_scaling_efficiency": base / (P * t)}
+        row = {"P": P, "heads_per_rank": H // P, "ms_per_rank_max": t, "ms_per_rank": times,
+               "rounds": a.rounds, "predicted_scaling_efficiency": base / (P * t)}
         rows.append(row)
         print(json.dumps(row), flush=True)
         if fout:
             fout.write(json.dumps(row) + "\n")
-
 
 def run_layers(a):
     dev = torch.device("cuda", 0)
@@ -244,6 +257,7 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--rounds", type=int, default=5, help="heads mode: interleaved timing rounds (median)")
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--sel-flags", type=int, default=0, help="NEXT-4 selection variants (layers mode)")
     ap.add_argument("--schedule", default=None, help="layers mode: budgets = d_hat of a profiler schedule JSON")
