@@ -48,8 +48,12 @@ __device__ __forceinline__ int smid() {
   if (threadIdx.x == 0 && blockIdx.y * gridDim.x + blockIdx.x < 65536) g_cta[blockIdx.y * gridDim.x + blockIdx.x][e] = (v)
 #define CS_CTA_W(e, v) \
   if ((threadIdx.x & 31) == 0 && blockIdx.y * gridDim.x + blockIdx.x < 65536) g_cta[blockIdx.y * gridDim.x + blockIdx.x][e] = (v)
+#ifdef CS_ATTN_TRACE  // per-event trace of CTA (0, 0): a branch + clock64 in the hot loop of every CTA
 #define CS_TRACE(e, j) \
   if (blockIdx.x == 0 && blockIdx.y == 0 && (threadIdx.x & 31) == 0 && (j) < 4096) g_trace[e][j] = clock64()
+#else
+#define CS_TRACE(e, j)
+#endif
 #else
 #define CS_TRACE(e, j)
 #define CS_CTA(e, v)
