@@ -234,6 +234,175 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// One-chunk form (ks <= 128, the query side) with hi and lo concatenated along N instead of K: the
+// B operand of a K = 16 step is the 2 nch rows [W_hi ; W_lo] (two TMA boxes of the same Wsplit rows,
+// columns s 64.. and D + s 64..), so each token tile takes D / 16 MMAs of N = 2 nch instead of 2 D / 16
+// of N = nch: the X tile is read from shared memory once per K-step instead of twice, and the
+// instructions are wide enough to reach the tensor floor (an SS instruction at N <= 128 costs
+// ~80 cycles whatever N is, scripts/micro/mma_shapes.cu).  score_j = acc[j] + acc[nch + j] (+ bias),
+// then the same grouped argmax.  TMEM: one 2 nch <= 256-column accumulator per token tile (the two
+// tiles of a unit: tile 0's epilogue overlaps tile 1's MMAs and tile 1's the next unit's tile 0).
+// W (2 slabs of 2 nch x 64 columns) stays resident across a head's units.
+// ---------------------------------------------------------------------------------------------
+template <int D>
+struct SmemNC {
+  static constexpr int HALVES = D / 64;
+  static constexpr int XT = BM * D * 2;
+  static constexpr int HALF_X = BM * 128;
+  static constexpr int XSTAGE = TILES * XT;
+  static constexpr int SLAB = 2 * NCH_MAX * 128;  // 64 columns x (hi rows ; lo rows)
+  static constexpr int OFF_X = 0;
+  static constexpr int OFF_W = OFF_X + 2 * XSTAGE;
+  static constexpr int OFF_BAR = OFF_W + HALVES * SLAB;
+  // x_full[2], x_empty[2], w_full[HALVES], w_empty[HALVES], acc_full[2], acc_empty[2]
+  static constexpr int OFF_MISC = OFF_BAR + 8 * 16;
+  static constexpr int BYTES = OFF_MISC + 16;
+  static constexpr int ALLOC = BYTES + 1024;
+};
+
+template <int D, bool BIAS>
+__global__ void __launch_bounds__(NTHREADS, 1)
+    k_assign_nc(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_w,
+                int H, int N, int ks, int nch, int ks_pad, int units_per_head, int num_units,
+                const float* __restrict__ bias, int32_t* __restrict__ labels) {
+  using L = SmemNC<D>;
+  constexpr int SLABS = L::HALVES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::OFF_BAR);
+  uint64_t* x_full = bars;
+  uint64_t* x_empty = bars + 2;
+  uint64_t* w_full = bars + 4;
+  uint64_t* w_empty = bars + 4 + SLABS;
+  uint64_t* acc_full = bars + 4 + 2 * SLABS;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + L::OFF_MISC);
+
+  const int warp = warp_id(), lane = lane_id();
+  const int upc = (num_units + gridDim.x - 1) / gridDim.x;
+  const int u_begin = blockIdx.x * upc, u_end = min(num_units, u_begin + upc);
+  const int slab_bytes = 2 * nch * 128;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < 2; ++s) { mbar_init(x_full + s, 1); mbar_init(x_empty + s, 1); }
+    for (int s = 0; s < SLABS; ++s) { mbar_init(w_full + s, 1); mbar_init(w_empty + s, 1); }
+    for (int t = 0; t < 2; ++t) { mbar_init(acc_full + t, 1); mbar_init(acc_empty + t, BM); }
+    fence_barrier_init();
+  }
+  if (warp == WARP_MMA) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == WARP_PRODUCER) {
+    if (lane == 0) {
+      tma_prefetch_desc(&tm_x);
+      tma_prefetch_desc(&tm_w);
+      int it = 0, prev_bh = -1;
+      for (int u = u_begin; u < u_end; ++u, ++it) {
+        const int bh = u / units_per_head, n0 = (u % units_per_head) * (TILES * BM);
+        const int b = bh / H, h = bh % H;
+        const int xs = it & 1;
+        mbar_wait(x_empty + xs, ((it >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(x_full + xs, L::XSTAGE);
+        for (int t = 0; t < TILES; ++t)
+          for (int hf = 0; hf < L::HALVES; ++hf)
+            tma_load_4d(sm + L::OFF_X + xs * L::XSTAGE + t * L::XT + hf * L::HALF_X, &tm_x, hf * 64,
+                        n0 + t * BM, h, b, x_full + xs);
+        for (int s = 0; s < SLABS; ++s) {
+          mbar_wait(w_empty + s, (it & 1) ^ 1);
+          if (bh == prev_bh) {
+            mbar_arrive(w_full + s);  // same head: the slab is still resident
+          } else {
+            mbar_arrive_expect_tx(w_full + s, slab_bytes);
+            uint8_t* dst = sm + L::OFF_W + s * L::SLAB;
+            tma_load_2d(dst, &tm_w, s * 64, bh * ks_pad, w_full + s);                  // W_hi rows
+            tma_load_2d(dst + nch * 128, &tm_w, D + s * 64, bh * ks_pad, w_full + s);  // W_lo rows
+          }
+        }
+        prev_bh = bh;
+      }
+    }
+  } else if (warp == WARP_MMA) {
+    if (lane == 0) {
+      const uint32_t idesc = idesc_bf16(BM, 2 * nch, 0, 0);
+      const uint32_t sX = smem_u32(sm + L::OFF_X), sW = smem_u32(sm + L::OFF_W);
+      int it = 0, gt = 0;
+      for (int u = u_begin; u < u_end; ++u, ++it) {
+        const int xs = it & 1;
+        mbar_wait(x_full + xs, (it >> 1) & 1);
+        for (int s = 0; s < SLABS; ++s) mbar_wait(w_full + s, it & 1);
+        tc_fence_after();
+        for (int t = 0; t < TILES; ++t, ++gt) {
+          mbar_wait(acc_empty + t, ((gt >> 1) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t d_tmem = tmem + t * 256;
+          for (int s = 0; s < SLABS; ++s) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const uint64_t ad = smem_desc_sw128(sX + xs * L::XSTAGE + t * L::XT + s * L::HALF_X + k * 32, 16, 1024);
+              const uint64_t bd = smem_desc_sw128(sW + s * L::SLAB + k * 32, 16, 1024);
+              mma_ss(d_tmem, ad, bd, idesc, (s > 0 || k > 0) ? 1u : 0u);
+            }
+          }
+          mma_commit(acc_full + t);
+        }
+        for (int s = 0; s < SLABS; ++s) mma_commit(w_empty + s);
+        mma_commit(x_empty + xs);
+      }
+    }
+    __syncwarp();
+  } else {
+    // epilogue: tile t = warp / 4; score_j = hi part + lo part (+ bias), grouped running argmax
+    const int t = warp >> 2, quad = warp & 3;
+    const int r = quad * 32 + lane;
+    const uint32_t t_acc = tmem + ((uint32_t)(quad * 32) << 16) + t * 256;
+    int gt = t;
+    for (int u = u_begin; u < u_end; ++u, gt += TILES) {
+      const int bh = u / units_per_head, n0 = (u % units_per_head) * (TILES * BM);
+      float best = -INFINITY;
+      int best_j = 0;
+      float keep[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) keep[i] = -INFINITY;
+      const float* bias_row = BIAS ? bias + (size_t)bh * ks_pad : nullptr;
+      mbar_wait(acc_full + t, (gt >> 1) & 1);
+      tc_fence_after();
+      for (int c0 = 0; c0 < nch; c0 += 16) {
+        uint32_t vh[16], vl[16];
+        float bs[16];
+        tmem_ld16(t_acc + c0, vh);
+        tmem_ld16(t_acc + nch + c0, vl);
+        if constexpr (BIAS) {
+          const float4* b4 = reinterpret_cast<const float4*>(bias_row + c0);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float4 q = __ldg(b4 + i);
+            bs[4 * i] = q.x; bs[4 * i + 1] = q.y; bs[4 * i + 2] = q.z; bs[4 * i + 3] = q.w;
+          }
+        }
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 16; ++i) vh[i] = __float_as_uint(__uint_as_float(vh[i]) + __uint_as_float(vl[i]));
+        argmax_group<BIAS>(vh, bs, c0, ks, best, best_j, keep);
+      }
+      tc_fence_before();
+      mbar_arrive(acc_empty + t);
+      best_j = argmax_finish(best, best_j, keep);
+      const int n = n0 + t * BM + r;
+      if (n < N) labels[(size_t)bh * N + n] = best_j;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == WARP_MMA) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
 }  // namespace asg
 
 // ---------------------------------------------------------------------------------------------
@@ -466,6 +635,27 @@ cudaError_t launch_assign_gemm(const CUtensorMap* tm_x, const CUtensorMap* tm_w,
     return cudaGetLastError();
   }
   const int grid = num_units < num_sms ? num_units : num_sms;
+#ifndef CS_ASSIGN_NC
+#define CS_ASSIGN_NC 1
+#endif
+  if (CS_ASSIGN_NC && ks_pad == nch && 2 * nch <= 256) {
+    auto launch_nc = [&](auto kfn, int smem) -> cudaError_t {
+      cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e != cudaSuccess) return e;
+      kfn<<<grid, asg::NTHREADS, smem, st>>>(*tm_x, *tm_w, H, N, ks, nch, ks_pad, units_per_head, num_units, bias,
+                                             labels);
+      return cudaSuccess;
+    };
+    cudaError_t e;
+    if (d == 128)
+      e = bias ? launch_nc(asg::k_assign_nc<128, true>, asg::SmemNC<128>::ALLOC)
+               : launch_nc(asg::k_assign_nc<128, false>, asg::SmemNC<128>::ALLOC);
+    else
+      e = bias ? launch_nc(asg::k_assign_nc<64, true>, asg::SmemNC<64>::ALLOC)
+               : launch_nc(asg::k_assign_nc<64, false>, asg::SmemNC<64>::ALLOC);
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+  }
   auto launch = [&](auto kfn, int smem) -> cudaError_t {
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
