@@ -508,8 +508,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
         const bool warp_rescale = __any_sync(0xffffffffu, alpha != 1.f);
         // p = 2^(s*scale_log2 - m): paired FFMA2, MUFU ex2, 4 independent FADD2 row-sum chains.
-        // Each 64-key half of P is stored and signalled as soon as it is done, so PV on the
-        // first half overlaps the exponentials of the second.
+        // P is stored and signalled in three parts (keys 0-63 and 64-95 to TMEM, 96-127 to SMEM):
+        // PV on the first part overlaps the exponentials of the rest, and QK(j+1) is issued as
+        // soon as the TMEM parts have been consumed.
         const float2 sl2 = make_float2(scale_log2, scale_log2), nm2 = make_float2(-m, -m);
         float2 acc4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
