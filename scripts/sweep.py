@@ -172,6 +172,8 @@ def run_heads(a):
             keys.reverse()
         for key in keys:
             call = calls[key]
+            for _ in range(2):  # re-warm after switching configurations (L2 / TLB state)
+                call()
             torch.cuda.synchronize()
             e0.record()
             for _ in range(a.steps):
