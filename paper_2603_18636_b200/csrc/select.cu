@@ -1,6 +1,7 @@
 // select.cu — top block-pair selection and the attention work list.
 //   k_select_rows : per (bh, query block a): Abar_a = C_q[a] C_k^T (fp64, empty key blocks -> -inf),
-//                   order = key blocks by (Abar desc, index asc) (bitonic sort in SMEM),
+//                   order = key blocks by (Abar desc, index asc) (bitonic sort of 32-bit keys,
+//                   exact fix-up of truncated-key collisions),
 //                   c_a = min{m : cumsum of softmax(Abar_a / sqrt(d)) over that order >= tau-1e-12}
 //   k_select_count: per bh: n_rec = ceil(sum c_a / Kq'), rule (R8, R10) -> n_keep
 //   k_select_emit : kept[a] = the first n_keep of order[a], ascending
@@ -10,63 +11,6 @@
 #include "kernels.cuh"
 
 namespace cs {
-
-__device__ __forceinline__ bool before(double va, int ia, double vb, int ib) {
-  return va > vb || (va == vb && ia < ib);
-}
-
-// Block-wide bitonic sort of P2 (power of two, 256 E <= P2 <= 1024... any P2 = 256 E) entries by
-// (value desc, index asc).  Thread t holds the E consecutive entries t E .. t E + E - 1 in
-// registers: strides < E are resolved inside the thread, strides < 32 E with warp shuffles,
-// and only the strides >= 32 E (6 stages at P2 = 512) go through shared memory.
-template <int E>
-__device__ void bitonic_sort_rows(double (&v)[E], int (&ix)[E], int P2, double* sval, int* sidx) {
-  const int t = threadIdx.x;
-  for (int size = 2; size <= P2; size <<= 1) {
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      if (stride < E) {
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          if (e & stride) continue;
-          const int e2 = e | stride;
-          const bool up = ((t * E + e) & size) == 0;
-          const bool sw = up ? before(v[e2], ix[e2], v[e], ix[e]) : before(v[e], ix[e], v[e2], ix[e2]);
-          if (sw) {
-            const double tv = v[e]; v[e] = v[e2]; v[e2] = tv;
-            const int ti = ix[e]; ix[e] = ix[e2]; ix[e2] = ti;
-          }
-        }
-      } else {
-        double vo[E];
-        int io[E];
-        if (stride < 32 * E) {
-#pragma unroll
-          for (int e = 0; e < E; ++e) {
-            vo[e] = __shfl_xor_sync(0xffffffffu, v[e], stride / E);
-            io[e] = __shfl_xor_sync(0xffffffffu, ix[e], stride / E);
-          }
-        } else {
-#pragma unroll
-          for (int e = 0; e < E; ++e) { sval[t * E + e] = v[e]; sidx[t * E + e] = ix[e]; }
-          __syncthreads();
-#pragma unroll
-          for (int e = 0; e < E; ++e) { vo[e] = sval[(t * E + e) ^ stride]; io[e] = sidx[(t * E + e) ^ stride]; }
-          __syncthreads();
-        }
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          const int i = t * E + e;
-          const bool lower = (i & stride) == 0, up = (i & size) == 0;
-          const bool take = (lower == up) ? before(vo[e], io[e], v[e], ix[e]) : before(v[e], ix[e], vo[e], io[e]);
-          if (take) { v[e] = vo[e]; ix[e] = io[e]; }
-        }
-      }
-    }
-  }
-#pragma unroll
-  for (int e = 0; e < E; ++e) { sval[t * E + e] = v[e]; sidx[t * E + e] = ix[e]; }
-  __syncthreads();
-}
 
 // Abar = C_q C_k^T in fp64.  grid (ceil(kk/64), ceil(kq/64), BH), block 256, dyn smem
 // 2 x 64 x (64+1) doubles: a 64 x 64 output tile; thread (ta, tj) = (t / 16, t % 16) owns the
@@ -128,7 +72,68 @@ __global__ void __launch_bounds__(256) k_abar(int kq, int kk, const float* __res
   }
 }
 
-// grid (kq, BH), block 256, dyn smem: P2 doubles + P2 ints + d doubles; P2 = 256 E
+// Order-preserving 32-bit sort key of (value desc, index asc): the value rounded to float (round to
+// nearest is monotone non-decreasing; -0 folded into +0 so that the two zeros, equal as doubles,
+// tie), its sign-flipped bits truncated to 22 bits (still monotone), then 1023 - j in the low 10
+// bits (K_k <= 1024), so that a larger key comes first and equal truncated values fall back to the
+// lower index.  Distinct doubles whose truncated keys collide are put back into exact order after
+// the sort (fixup_runs); all other pairs are already ordered exactly.
+__device__ __forceinline__ uint32_t sort_key(double v, int j) {
+  const float f = __double2float_rn(v) + 0.0f;
+  uint32_t u = __float_as_uint(f);
+  u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+  return ((u >> 10) << 10) | (uint32_t)(1023 - j);
+}
+__device__ __forceinline__ int key_index(uint32_t k) { return 1023 - (int)(k & 1023u); }
+
+// Block-wide bitonic sort (descending) of P2 = 256 E distinct 32-bit keys.  Thread t holds the E
+// consecutive entries t E .. t E + E - 1 in registers: strides < E are resolved inside the thread,
+// strides < 32 E with warp shuffles, and only the strides >= 32 E go through shared memory.
+template <int E>
+__device__ void bitonic_sort_keys(uint32_t (&k)[E], int P2, uint32_t* skey) {
+  const int t = threadIdx.x;
+  for (int size = 2; size <= P2; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      if (stride < E) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          if (e & stride) continue;
+          const int e2 = e | stride;
+          const bool up = ((t * E + e) & size) == 0;
+          const uint32_t a = k[e], b = k[e2];
+          const bool sw = up ? (b > a) : (a > b);
+          k[e] = sw ? b : a;
+          k[e2] = sw ? a : b;
+        }
+      } else {
+        uint32_t ko[E];
+        if (stride < 32 * E) {
+#pragma unroll
+          for (int e = 0; e < E; ++e) ko[e] = __shfl_xor_sync(0xffffffffu, k[e], stride / E);
+        } else {
+#pragma unroll
+          for (int e = 0; e < E; ++e) skey[t * E + e] = k[e];
+          __syncthreads();
+#pragma unroll
+          for (int e = 0; e < E; ++e) ko[e] = skey[(t * E + e) ^ stride];
+          __syncthreads();
+        }
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int i = t * E + e;
+          const bool lower = (i & stride) == 0, up = (i & size) == 0;
+          // keep the larger key where (lower == up), the smaller one elsewhere
+          k[e] = (lower == up) ? max(k[e], ko[e]) : min(k[e], ko[e]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < E; ++e) skey[t * E + e] = k[e];
+  __syncthreads();
+}
+
+// grid (kq, BH), block 256, dyn smem: 2 P2 doubles + P2 uint32; P2 = 256 E
 template <int E>
 __global__ void __launch_bounds__(256) k_select_rows(int kq, int kk, int d, const double* __restrict__ abar,
                                                      const int32_t* __restrict__ offs_q,
@@ -139,29 +144,64 @@ __global__ void __launch_bounds__(256) k_select_rows(int kq, int kk, int d, cons
   __shared__ double wred[8];
   __shared__ int first_hit;
   constexpr int P2 = 256 * E;
-  double* sval = sh_d;
-  double* scq = sh_d + P2;
-  int* sidx = reinterpret_cast<int*>(scq + d);
+  double* sval = sh_d;                 // [P2] values in sorted order
+  double* vbyj = sh_d + P2;            // [P2] values by key-block index
+  uint32_t* skey = reinterpret_cast<uint32_t*>(vbyj + P2);  // [P2] sorted keys
   const int a = blockIdx.x, bh = blockIdx.y, t = threadIdx.x;
   const int32_t* ok = offs_k + (size_t)bh * (kk + 1);
   const int32_t* oq = offs_q + (size_t)bh * (kq + 1);
-  (void)scq;
   const double* arow = abar + ((size_t)bh * kq + a) * kk;
   // sort: (value desc, index asc); empty key blocks and padding are -inf.  The value is the raw
   // Abar (R7), or with CS_SEL_SIZE_WEIGHTED the importance Abar / sqrt(d) + log|K_c| (R9c).
   const double sdiv = weighted ? 1.0 : sqrt((double)d);  // softmax argument = value / sdiv
   {
-    double v[E];
-    int ix[E];
+    uint32_t key[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       const int j = t * E + e;
       const int sz = j < kk ? ok[j + 1] - ok[j] : 0;
-      v[e] = sz > 0 ? (weighted ? arow[j] / sqrt((double)d) + log((double)sz) : arow[j]) : -INFINITY;
-      ix[e] = j;
+      const double v = sz > 0 ? (weighted ? arow[j] / sqrt((double)d) + log((double)sz) : arow[j]) : -INFINITY;
+      vbyj[j] = v;
+      key[e] = sort_key(v, j);
     }
-    bitonic_sort_rows<E>(v, ix, P2, sval, sidx);
+    bitonic_sort_keys<E>(key, P2, skey);
   }
+#pragma unroll
+  for (int e = 0; e < E; ++e) sval[t * E + e] = vbyj[key_index(skey[t * E + e])];
+  __syncthreads();
+  // fixup_runs: a run of equal truncated keys holding distinct values is re-ordered exactly by
+  // (value desc, index asc) by the thread owning its first entry (insertion sort; runs are short
+  // and rare, and a run of equal values is already in index order).  The runs are found before any
+  // thread reorders one (reads and writes of the arrays in separate phases).
+  int run_b[E], run_e[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int i = t * E + e;
+    const uint32_t hk = skey[i] >> 10;
+    run_b[e] = run_e[e] = i;
+    if (i + 1 >= P2 || (skey[i + 1] >> 10) != hk || (i > 0 && (skey[i - 1] >> 10) == hk)) continue;
+    int r = i + 1;
+    while (r < P2 && (skey[r] >> 10) == hk) ++r;
+    run_e[e] = r;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int i = run_b[e], r = run_e[e];
+    for (int x = i + 1; x < r; ++x) {
+      const uint32_t kx = skey[x];
+      const double vx = sval[x];
+      int y = x - 1;
+      while (y >= i && (sval[y] < vx || (sval[y] == vx && key_index(skey[y]) > key_index(kx)))) {
+        skey[y + 1] = skey[y];
+        sval[y + 1] = sval[y];
+        --y;
+      }
+      skey[y + 1] = kx;
+      sval[y + 1] = vx;
+    }
+  }
+  __syncthreads();
   // number of nonempty key blocks
   int ne = 0;
   for (int j = t; j < kk; j += 256) ne += (ok[j + 1] - ok[j] > 0) ? 1 : 0;
@@ -172,7 +212,7 @@ __global__ void __launch_bounds__(256) k_select_rows(int kq, int kk, int d, cons
   int kne = 0;
   for (int w = 0; w < 8; ++w) kne += sne[w];
   int32_t* ord = order + ((size_t)bh * kq + a) * kk;
-  for (int j = t; j < kk; j += 256) ord[j] = sidx[j];
+  for (int j = t; j < kk; j += 256) ord[j] = key_index(skey[j]);
   const bool q_nonempty = oq[a + 1] - oq[a] > 0;
   if (!q_nonempty || kne == 0) {
     if (t == 0) cnt[(size_t)bh * kq + a] = 0;
@@ -350,7 +390,7 @@ cudaError_t launch_block_select(int BH, int H, int kq, int kk, int d, const floa
   const int weighted = (flags & 2) ? 1 : 0;
   int P2 = 256;
   while (P2 < kk) P2 <<= 1;
-  const size_t smem = (size_t)P2 * 8 + (size_t)d * 8 + (size_t)P2 * 4;
+  const size_t smem = (size_t)P2 * 16 + (size_t)P2 * 4;
   const dim3 gab((kk + 63) / 64, (kq + 63) / 64, BH);
   constexpr int sab = 2 * 64 * 65 * 8;  // > 48 KB: opt in
   if (d == 128) {

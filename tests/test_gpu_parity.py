@@ -257,6 +257,50 @@ def test_block_select_variants_bitexact(pb, flags, rule, kq, kk, d, tau):
             assert np.array_equal(kept[0, h, a, :rows[a]].cpu().numpy(), np.asarray(ref.kept[a]))
 
 
+@pytest.mark.parametrize("kk", [300, 1000, 1024])
+def test_block_select_exact_ties_and_float_collisions(pb, kk):
+    """The selection order is (Abar desc, index asc) over exact float64 values (R11, R2).
+    The kernel sorts 32-bit keys (value rounded to float, 22 bits) and puts colliding distinct
+    values back into exact order; this case is built so that collisions and exact ties are the
+    common case: Abar[a, j] = c_j + delta_j exactly (query rows e_0 + e_1, key rows (c_j, delta_j,
+    0, ...)), c_j from a few float values and delta_j in {0, 1, 2, 3} * 2^-40, below half a float
+    ulp of c_j — so every c_j group is one float key with up to four distinct doubles, each repeated
+    (exact ties -> lower index).  Eight heads with the same rows and keep ratios spread over (0, 1)
+    cut the order at many places; the FIXED kept sets pin the order, the DENSITY counts the
+    recall prefix."""
+    H, kq, d = 8, 3, 64
+    g = torch.Generator().manual_seed(kk)
+    cvals = torch.tensor([1.0, 1.5, 0.75, -0.5, 0.0, 1.25])
+    c = cvals[torch.randint(0, len(cvals), (kk,), generator=g)]
+    delta = torch.randint(0, 4, (kk,), generator=g).double() * 2.0 ** -40
+    Ck = torch.zeros(kk, d, dtype=torch.float64)
+    Ck[:, 0] = c.double()
+    Ck[:, 1] = delta
+    Cq = torch.zeros(kq, d, dtype=torch.float64)
+    Cq[:, 0] = 1.0
+    Cq[:, 1] = 1.0
+    Cq[1, 0] = 2.0  # another exact row: 2 c_j + delta_j
+    assert torch.equal(Ck.float().double(), Ck) and torch.equal(Cq.float().double(), Cq)
+    sq = torch.ones(H, kq, dtype=torch.long)
+    sk = torch.randint(1, 4, (H, kk), generator=g)
+    sk[:, 5] = 0  # an empty key block is never eligible
+    sk[:] = sk[0]
+    offs_q = torch.cat([torch.zeros(H, 1, dtype=torch.long), sq.cumsum(1)], 1).int()[None]
+    offs_k = torch.cat([torch.zeros(H, 1, dtype=torch.long), sk.cumsum(1)], 1).int()[None]
+    budget = torch.tensor([0.01, 0.07, 0.13, 0.2, 0.33, 0.5, 0.77, 0.99], dtype=torch.float32)
+    Cqh = Cq.float()[None, None].expand(1, H, kq, d).contiguous()
+    Ckh = Ck.float()[None, None].expand(1, H, kk, d).contiguous()
+    for rule in (svoo.RULE_FIXED, svoo.RULE_DENSITY):
+        n_keep, kept = pb.block_select(Cqh.cuda(), Ckh.cuda(), offs_q.cuda(), offs_k.cuda(), budget.cuda(),
+                                       0.9, 0.1, rule)
+        torch.cuda.synchronize()
+        for h in range(H):
+            ref = svoo.select_blocks(Cq.numpy(), Ck.numpy(), sq[h].numpy(), sk[h].numpy(), float(budget[h]),
+                                     0.9, 0.1, rule, d_head=d)
+            assert n_keep[0, h].item() == ref.n_keep, (rule, h)
+            assert np.array_equal(kept[0, h, :, :ref.n_keep].cpu().numpy(), ref.kept), (rule, h)
+
+
 def test_attn_per_row_counts_and_fused_variants(pb):
     """Attention over per-row kept counts (R11b) against the oracle, and the fused entry with
     selection flags bit-equal to the staged entries."""
