@@ -78,6 +78,7 @@ __global__ void __launch_bounds__(256) k_abar(int kq, int kk, const float* __res
 // bits (K_k <= 1024), so that a larger key comes first and equal truncated values fall back to the
 // lower index.  Distinct doubles whose truncated keys collide are put back into exact order after
 // the sort (fixup_runs); all other pairs are already ordered exactly.
+static_assert(kMaxClusters <= 1024, "sort_key packs the key-block index into 10 bits");
 __device__ __forceinline__ uint32_t sort_key(double v, int j) {
   const float f = __double2float_rn(v) + 0.0f;
   uint32_t u = __float_as_uint(f);
