@@ -139,7 +139,7 @@ template <int E>
 __global__ void __launch_bounds__(256) k_select_rows(int kq, int kk, int d, const double* __restrict__ abar,
                                                      const int32_t* __restrict__ offs_q,
                                                      const int32_t* __restrict__ offs_k, double tau,
-                                                     int weighted, int32_t* __restrict__ order,
+                                                     int weighted, int need_cnt, int32_t* __restrict__ order,
                                                      int32_t* __restrict__ cnt) {
   extern __shared__ double sh_d[];
   __shared__ double wred[8];
@@ -203,6 +203,13 @@ __global__ void __launch_bounds__(256) k_select_rows(int kq, int kk, int d, cons
     }
   }
   __syncthreads();
+  int32_t* ord = order + ((size_t)bh * kq + a) * kk;
+  for (int j = t; j < kk; j += 256) ord[j] = key_index(skey[j]);
+  // the FIXED rule keeps n_b blocks whatever the recall counts are: c_a is not computed
+  if (!need_cnt) {
+    if (t == 0) cnt[(size_t)bh * kq + a] = 0;
+    return;
+  }
   // number of nonempty key blocks
   int ne = 0;
   for (int j = t; j < kk; j += 256) ne += (ok[j + 1] - ok[j] > 0) ? 1 : 0;
@@ -212,8 +219,6 @@ __global__ void __launch_bounds__(256) k_select_rows(int kq, int kk, int d, cons
   __syncthreads();
   int kne = 0;
   for (int w = 0; w < 8; ++w) kne += sne[w];
-  int32_t* ord = order + ((size_t)bh * kq + a) * kk;
-  for (int j = t; j < kk; j += 256) ord[j] = key_index(skey[j]);
   const bool q_nonempty = oq[a + 1] - oq[a] > 0;
   if (!q_nonempty || kne == 0) {
     if (t == 0) cnt[(size_t)bh * kq + a] = 0;
@@ -389,6 +394,7 @@ cudaError_t launch_block_select(int BH, int H, int kq, int kk, int d, const floa
                                 int32_t* n_keep, int32_t* n_rows, int32_t* kept, int32_t* order,
                                 int32_t* cnt, double* abar, cudaStream_t st) {
   const int weighted = (flags & 2) ? 1 : 0;
+  const int need_cnt = rule != 2;  // FIXED (rule 2): n = n_b for every row, the recall counts are unused
   int P2 = 256;
   while (P2 < kk) P2 <<= 1;
   const size_t smem = (size_t)P2 * 16 + (size_t)P2 * 4;
@@ -404,11 +410,11 @@ cudaError_t launch_block_select(int BH, int H, int kq, int kk, int d, const floa
     k_abar<64><<<gab, 256, sab, st>>>(kq, kk, cq, ck, abar);
   }
   if (P2 == 256)
-    k_select_rows<1><<<dim3(kq, BH), 256, smem, st>>>(kq, kk, d, abar, offs_q, offs_k, tau, weighted, order, cnt);
+    k_select_rows<1><<<dim3(kq, BH), 256, smem, st>>>(kq, kk, d, abar, offs_q, offs_k, tau, weighted, need_cnt, order, cnt);
   else if (P2 == 512)
-    k_select_rows<2><<<dim3(kq, BH), 256, smem, st>>>(kq, kk, d, abar, offs_q, offs_k, tau, weighted, order, cnt);
+    k_select_rows<2><<<dim3(kq, BH), 256, smem, st>>>(kq, kk, d, abar, offs_q, offs_k, tau, weighted, need_cnt, order, cnt);
   else
-    k_select_rows<4><<<dim3(kq, BH), 256, smem, st>>>(kq, kk, d, abar, offs_q, offs_k, tau, weighted, order, cnt);
+    k_select_rows<4><<<dim3(kq, BH), 256, smem, st>>>(kq, kk, d, abar, offs_q, offs_k, tau, weighted, need_cnt, order, cnt);
   k_select_count<<<BH, 1024, 0, st>>>(H, kq, kk, offs_q, offs_k, cnt, budget, theta, rule, flags & 1, n_keep,
                                       n_rows);
   k_select_emit<<<dim3(kq, BH), 256, 0, st>>>(kq, kk, order, n_keep, n_rows, kept);
