@@ -80,8 +80,8 @@ __global__ void __launch_bounds__(256) k_abar(int kq, int kk, const float* __res
 // the sort (fixup_runs); all other pairs are already ordered exactly.
 static_assert(kMaxClusters <= 1024, "sort_key packs the key-block index into 10 bits");
 __device__ __forceinline__ uint32_t sort_key(double v, int j) {
-  const float f = __double2float_rn(v) + 0.0f;
-  uint32_t u = __float_as_uint(f);
+  uint32_t u = __float_as_uint(__double2float_rn(v));
+  if ((u << 1) == 0u) u = 0u;  // -0 -> +0 (bitwise, so no compiler flag can fold it away)
   u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
   return ((u >> 10) << 10) | (uint32_t)(1023 - j);
 }
