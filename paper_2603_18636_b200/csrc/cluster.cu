@@ -198,14 +198,14 @@ __device__ __forceinline__ __nv_bfloat16 to_bf16(float v) { return __float2bfloa
 // the two halves the same ones (broadcast).
 // Rows of C_a are staged in fp64 chunks of 32; per staged row 8 LDS.64 feed 16 DFMA.
 // ---------------------------------------------------------------------------------------------
-template <int D>
+template <int D, int TB>
 __global__ void __launch_bounds__(256) k_gamma(const float* __restrict__ ca, int ka,
                                                prep_t* __restrict__ gamma) {
   // split over the anchor rows: CTA z sums rows [z GR, (z+1) GR) into the partial Gamma_z (a
   // [gridDim.z][BH][D][D] slab); k_gamma_reduce adds the partials into slab 0 in a fixed order.
   // Short serial loops keep the kernel off the latency floor when few heads share a launch
   // (head-parallel ranks).
-  constexpr int CH = 32, TB = 64, NB = D / TB, GR = kGammaRows;
+  constexpr int CH = 32, NB = D / TB, GR = kGammaRows, RT = TB / 16;  // RT x RT outputs per thread
   __shared__ __align__(16) prep_t sa[CH][D];
   // upper-triangle block index -> (row block, column block), column block >= row block
   int rb = 0, cb = blockIdx.y;
@@ -216,11 +216,11 @@ __global__ void __launch_bounds__(256) k_gamma(const float* __restrict__ ca, int
   const float* A = ca + (size_t)bh * ka * D;
   gamma += (size_t)blockIdx.z * gridDim.x * D * D;
   const int t = threadIdx.x, ti = t >> 4, tj = t & 15;
-  prep_t acc[4][4];
+  prep_t acc[RT][RT];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < RT; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = prep_t(0);
+    for (int j = 0; j < RT; ++j) acc[i][j] = prep_t(0);
   for (int a0 = r_beg; a0 < r_end; a0 += CH) {
     const int n = min(CH, r_end - a0);
     __syncthreads();
@@ -231,25 +231,25 @@ __global__ void __launch_bounds__(256) k_gamma(const float* __restrict__ ca, int
     }
     __syncthreads();
     for (int r = 0; r < n; ++r) {
-      prep_t ve[4], vf[4];
+      prep_t ve[RT], vf[RT];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) { ve[i] = sa[r][e0 + ti + 16 * i]; vf[i] = sa[r][f0 + tj + 16 * i]; }
+      for (int i = 0; i < RT; ++i) { ve[i] = sa[r][e0 + ti + 16 * i]; vf[i] = sa[r][f0 + tj + 16 * i]; }
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < RT; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fma(ve[i], vf[j], acc[i][j]);
+        for (int j = 0; j < RT; ++j) acc[i][j] = fma(ve[i], vf[j], acc[i][j]);
     }
   }
   prep_t* G = gamma + (size_t)bh * D * D;
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < RT; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) G[(size_t)(e0 + ti + 16 * i) * D + f0 + tj + 16 * j] = acc[i][j];
+    for (int j = 0; j < RT; ++j) G[(size_t)(e0 + ti + 16 * i) * D + f0 + tj + 16 * j] = acc[i][j];
   if (rb != cb) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < RT; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) G[(size_t)(f0 + tj + 16 * j) * D + e0 + ti + 16 * i] = acc[i][j];
+      for (int j = 0; j < RT; ++j) G[(size_t)(f0 + tj + 16 * j) * D + e0 + ti + 16 * i] = acc[i][j];
   }
 }
 
@@ -274,11 +274,12 @@ __global__ void __launch_bounds__(256) k_gamma_reduce(prep_t* __restrict__ gamma
 // consecutive lanes read consecutive Gamma columns).  Gamma is streamed through shared memory in chunks of 32 rows.  Rows j >= ks
 // are written as zeros (padding).
 // ---------------------------------------------------------------------------------------------
-template <int D>
+template <int D, int J>
 __global__ void __launch_bounds__(256) k_anchor_w(const float* __restrict__ cs_, int ks, int ks_pad,
                                                   const prep_t* __restrict__ gamma,
                                                   __nv_bfloat16* __restrict__ wsplit) {
-  constexpr int J = 32, EG = D / 4, JG = 256 / EG, JPT = J / JG, FCH = 32;
+  constexpr int EG = D / 4, JG = 256 / EG, JPT = J / JG, FCH = 32;
+  static_assert(JPT >= 1, "at least one centroid per thread");
   extern __shared__ __align__(16) prep_t sm_aw[];
   prep_t (*sc)[D] = reinterpret_cast<prep_t (*)[D]>(sm_aw);           // [J][D]   centroids
   prep_t (*sg)[D] = reinterpret_cast<prep_t (*)[D]>(sm_aw + J * D);   // [FCH][D] Gamma rows
@@ -634,23 +635,43 @@ cudaError_t launch_init_sample(XView q, XView k, int BH, int N, int d, int kq, i
   return cudaGetLastError();
 }
 
+// Output tiling of the two prep kernels: Gamma in 64 x 64 blocks and W in 32 centroids per CTA, or
+// finer tiles when a launch would not fill one wave of the SMs (few heads per call: head-parallel
+// ranks, small models).  Every output keeps its own sequential summation order, so the choice
+// does not change a single bit (and head-sharded calls stay bit-equal to unsharded ones).
 cudaError_t launch_anchor_prep(const float* ca, int ka, const float* cself, int ks, int ks_pad,
                                int BH, int d, void* gamma_ws, __nv_bfloat16* wsplit, cudaStream_t st) {
   prep_t* gamma = static_cast<prep_t*>(gamma_ws);
   const int nparts = (ka + kGammaRows - 1) / kGammaRows;  // gamma holds nparts x BH x d x d
   const size_t slab = (size_t)BH * d * d;
-  if (d == 128) {
-    constexpr int smem = 2 * 32 * 128 * (int)sizeof(prep_t);
-    cudaError_t e = cudaFuncSetAttribute(k_anchor_w<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  int num_sms = 0, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+  if (num_sms <= 0) num_sms = 148;
+  const int nb64 = d / 64, nb32 = d / 32;
+  const bool g_fine = BH * nparts * (nb64 * (nb64 + 1) / 2) < num_sms;  // 32 x 32 Gamma blocks
+  const int jw = ((ks_pad + 31) / 32) * BH >= num_sms ? 32 : (((ks_pad + 15) / 16) * BH >= num_sms || d == 64 ? 16 : 8);
+  auto launch_w = [&](auto kfn, int J) -> cudaError_t {
+    const int smem = (J + 32) * d * (int)sizeof(prep_t);
+    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    k_gamma<128><<<dim3(BH, 3, nparts), 256, 0, st>>>(ca, ka, gamma);
+    kfn<<<dim3((ks_pad + J - 1) / J, BH), 256, smem, st>>>(cself, ks, ks_pad, gamma, wsplit);
+    return cudaSuccess;
+  };
+  cudaError_t e;
+  if (d == 128) {
+    if (g_fine) k_gamma<128, 32><<<dim3(BH, nb32 * (nb32 + 1) / 2, nparts), 256, 0, st>>>(ca, ka, gamma);
+    else k_gamma<128, 64><<<dim3(BH, nb64 * (nb64 + 1) / 2, nparts), 256, 0, st>>>(ca, ka, gamma);
     if (nparts > 1) k_gamma_reduce<<<(unsigned)((slab / 2 + 255) / 256), 256, 0, st>>>(gamma, slab, nparts);
-    k_anchor_w<128><<<dim3((ks_pad + 31) / 32, BH), 256, smem, st>>>(cself, ks, ks_pad, gamma, wsplit);
+    e = jw == 32 ? launch_w(k_anchor_w<128, 32>, 32) : jw == 16 ? launch_w(k_anchor_w<128, 16>, 16)
+                                                                 : launch_w(k_anchor_w<128, 8>, 8);
   } else {
-    k_gamma<64><<<dim3(BH, 1, nparts), 256, 0, st>>>(ca, ka, gamma);
+    if (g_fine) k_gamma<64, 32><<<dim3(BH, nb32 * (nb32 + 1) / 2, nparts), 256, 0, st>>>(ca, ka, gamma);
+    else k_gamma<64, 64><<<dim3(BH, nb64 * (nb64 + 1) / 2, nparts), 256, 0, st>>>(ca, ka, gamma);
     if (nparts > 1) k_gamma_reduce<<<(unsigned)((slab / 2 + 255) / 256), 256, 0, st>>>(gamma, slab, nparts);
-    k_anchor_w<64><<<dim3((ks_pad + 31) / 32, BH), 256, 2 * 32 * 64 * (int)sizeof(prep_t), st>>>(cself, ks, ks_pad, gamma, wsplit);
+    e = jw == 32 ? launch_w(k_anchor_w<64, 32>, 32) : launch_w(k_anchor_w<64, 16>, 16);
   }
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
